@@ -1,0 +1,205 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY (ctypes wrapper over oracle/oracle.c).
+
+Plain CPU FP64 implementation of the paper's discrete quantities (Eqs. (5)-(14) of
+arXiv 1301.5885; see the header of oracle.c for the per-function citations) plus the
+closed forms in oracle/kirkwood.py.  Only tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / `--impl reference` legs may import this package.  It shares
+no code with the CUDA product path in paper_1301_5885_b200/.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+_D = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.c_int64
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("restarts", ctypes.c_int64), ("matvecs", ctypes.c_int64),
+                ("converged", ctypes.c_int64), ("rel_res_est", ctypes.c_double),
+                ("rel_res_true", ctypes.c_double), ("history", _D), ("history_cap", ctypes.c_int64),
+                ("history_len", ctypes.c_int64)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        d, i, p = ctypes.c_double, _I, _D
+        for name, args, res in [
+            ("orc_G0", [p, p], d), ("orc_Gk", [p, p, d], d),
+            ("orc_dG0_dny", [p, p, p], d), ("orc_dGk_dny", [p, p, p, d], d),
+            ("orc_dG0_dnx", [p, p, p], d), ("orc_dGk_dnx", [p, p, p, d], d),
+            ("orc_d2G0_dnxdny", [p, p, p, p], d), ("orc_d2Gk_dnxdny", [p, p, p, p, d], d),
+            ("orc_kernels", [p, p, p, p, d, d, p], None),
+            ("orc_source", [i, p, p, i, p, d, p], None),
+            ("orc_matvec", [i, p, p, p, d, d, p, p], None),
+            ("orc_matvec_rows", [i, p, p, p, d, d, p, i, ctypes.POINTER(_I), p], None),
+            ("orc_dense_assemble", [i, p, p, p, d, d, p], None),
+            ("orc_gmres_dense", [i, p, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
+            ("orc_gmres_bem", [i, p, p, p, d, d, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
+            ("orc_reaction_potential", [i, p, p, p, d, d, i, p, p, p], None),
+            ("orc_energy", [i, p, p, p, d, d, i, p, p, p], d),
+        ]:
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(_D)
+
+
+def _c(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def eps_ratio(eps1: float, eps2: float) -> float:
+    """eps = eps2/eps1 (reading R1 of DESIGN.md; P:247 prints the inverse)."""
+    return eps2 / eps1
+
+
+# ---------------------------------------------------------------- pair functions
+def G0(x, y):
+    return lib().orc_G0(_p(_c(x)), _p(_c(y)))
+
+
+def Gk(x, y, kappa):
+    return lib().orc_Gk(_p(_c(x)), _p(_c(y)), kappa)
+
+
+def dG0_dny(x, y, ny):
+    return lib().orc_dG0_dny(_p(_c(x)), _p(_c(y)), _p(_c(ny)))
+
+
+def dGk_dny(x, y, ny, kappa):
+    return lib().orc_dGk_dny(_p(_c(x)), _p(_c(y)), _p(_c(ny)), kappa)
+
+
+def dG0_dnx(x, nx, y):
+    return lib().orc_dG0_dnx(_p(_c(x)), _p(_c(nx)), _p(_c(y)))
+
+
+def dGk_dnx(x, nx, y, kappa):
+    return lib().orc_dGk_dnx(_p(_c(x)), _p(_c(nx)), _p(_c(y)), kappa)
+
+
+def d2G0_dnxdny(x, nx, y, ny):
+    return lib().orc_d2G0_dnxdny(_p(_c(x)), _p(_c(nx)), _p(_c(y)), _p(_c(ny)))
+
+
+def d2Gk_dnxdny(x, nx, y, ny, kappa):
+    return lib().orc_d2Gk_dnxdny(_p(_c(x)), _p(_c(nx)), _p(_c(y)), _p(_c(ny)), kappa)
+
+
+def kernels(x, nx, y, ny, eps, kappa):
+    K = np.zeros(4)
+    lib().orc_kernels(_p(_c(x)), _p(_c(nx)), _p(_c(y)), _p(_c(ny)), eps, kappa, _p(K))
+    return K
+
+
+# ---------------------------------------------------------------- direct sums
+def source(prob) -> np.ndarray:
+    b = np.zeros(2 * prob.n)
+    lib().orc_source(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), prob.nc,
+                     _p(_c(prob.charges)), prob.eps1, _p(b))
+    return b
+
+
+def matvec(prob, u) -> np.ndarray:
+    u = _c(u)
+    y = np.zeros(2 * prob.n)
+    lib().orc_matvec(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                     eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(u), _p(y))
+    return y
+
+
+def matvec_rows(prob, u, rows) -> tuple[np.ndarray, np.ndarray]:
+    """Rows i (and i+N) of A u for the given element indices: returns (y[i], y[i+N])."""
+    u = _c(u)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros(2 * rows.size)
+    lib().orc_matvec_rows(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                          eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(u), rows.size,
+                          rows.ctypes.data_as(ctypes.POINTER(_I)), _p(out))
+    return out[0::2].copy(), out[1::2].copy()
+
+
+def dense_assemble(prob) -> np.ndarray:
+    if prob.n > 3000:
+        raise ValueError("dense oracle capped at N <= 3000")
+    A = np.zeros((2 * prob.n, 2 * prob.n))
+    lib().orc_dense_assemble(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                             eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(A))
+    return A
+
+
+def _report(rep, hist):
+    return {"iterations": rep.iterations, "restarts": rep.restarts, "matvecs": rep.matvecs,
+            "converged": bool(rep.converged), "rel_res_est": rep.rel_res_est,
+            "rel_res_true": rep.rel_res_true, "history": hist[:min(rep.history_len, hist.size)].copy()}
+
+
+def gmres_dense(A, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True):
+    A, b = _c(A), _c(b)
+    m = b.size
+    x = np.zeros(m) if x0 is None else _c(x0).copy()
+    hist = np.zeros(max_iters + 1)
+    rep = Report(history=_p(hist), history_cap=hist.size)
+    st = lib().orc_gmres_dense(m, _p(A), _p(b), _p(x), restart, tol, max_iters, int(check_true),
+                               ctypes.byref(rep))
+    return x, st, _report(rep, hist)
+
+
+def gmres(prob, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True):
+    b = _c(b)
+    x = np.zeros(2 * prob.n) if x0 is None else _c(x0).copy()
+    hist = np.zeros(max_iters + 1)
+    rep = Report(history=_p(hist), history_cap=hist.size)
+    st = lib().orc_gmres_bem(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                             eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(b), _p(x), restart, tol,
+                             max_iters, int(check_true), ctypes.byref(rep))
+    return x, st, _report(rep, hist)
+
+
+def reaction_potential(prob, x) -> np.ndarray:
+    phi = np.zeros(prob.nc)
+    lib().orc_reaction_potential(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                                 eps_ratio(prob.eps1, prob.eps2), prob.kappa, prob.nc,
+                                 _p(_c(prob.charges)), _p(_c(x)), _p(phi))
+    return phi
+
+
+def energy(prob, x) -> float:
+    """E_sol in kcal/mol (Eq. (14); reading R3)."""
+    return lib().orc_energy(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+                            eps_ratio(prob.eps1, prob.eps2), prob.kappa, prob.nc, _p(_c(prob.charges)),
+                            _p(_c(x)), None)
+
+
+def solve(prob, restart=20, tol=1e-10, max_iters=500, check_true=True):
+    """Table 1 pipeline: source -> GMRES -> energy.  Returns a dict."""
+    b = source(prob)
+    x, st, rep = gmres(prob, b, None, restart, tol, max_iters, check_true)
+    e = energy(prob, x)
+    return {"b": b, "x": x, "status": st, "report": rep, "energy": e}

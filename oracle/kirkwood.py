@@ -1,0 +1,89 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.  Closed-form solvation energies for a dielectric
+sphere, the analytic references of PAPER.md §3.1-3.2 (P:104-106, 371-372, 420-422:
+"analytical solutions in terms of spherical harmonics are available [Kirkwood34]").
+
+The paper cites Kirkwood (1934) without printing coefficients; they are re-derived in
+SURVEY.md Appendix A.3 by matching phi and eps*dphi/dr on r = a order by order
+(interface conditions Eq. (3)):
+
+  E_sol = 1/2 C_E sum_k sum_l Q_k Q_l sum_n (|y_k||y_l|)^n / (eps1 a^(2n+1)) f_n P_n(cos g_kl)
+  f_n   = (eps2 g_n + (n+1) eps1) / (n eps1 - eps2 g_n),   g_n = x k_n'(x)/k_n(x), x = kappa a
+
+with k_n the modified spherical Bessel function of the second kind.  Units follow
+reading R3 (q = Q in e_c, C_E = 332.0716 kcal A / mol).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+C_E = 332.0716
+
+
+def born_energy(Q: float, a: float, eps1: float, eps2: float, kappa: float) -> float:
+    """Born ion with salt: 1/2 C_E Q^2/a [1/(eps2 (1+kappa a)) - 1/eps1]."""
+    return 0.5 * C_E * Q * Q / a * (1.0 / (eps2 * (1.0 + kappa * a)) - 1.0 / eps1)
+
+
+def g_ratio(nmax: int, x: float) -> np.ndarray:
+    """g_n = x k_n'(x)/k_n(x) for n = 0..nmax via the ratio R_n = k_{n-1}/k_n:
+    R_0 = 1 (k_{-1} = k_0), 1/R_{n+1} = R_n + (2n+1)/x, and g_n = -x R_n - (n+1)
+    (from k_n' = -k_{n-1} - (n+1) k_n / x).  For x = 0: g_n = -(n+1)."""
+    g = np.empty(nmax + 1)
+    if x == 0.0:
+        return -(np.arange(nmax + 1) + 1.0)
+    R = 1.0
+    for n in range(nmax + 1):
+        g[n] = -x * R - (n + 1.0)
+        R = 1.0 / (R + (2.0 * n + 1.0) / x)
+    return g
+
+
+def f_coeff(nmax: int, eps1: float, eps2: float, kappa: float, a: float) -> np.ndarray:
+    g = g_ratio(nmax, kappa * a)
+    n = np.arange(nmax + 1, dtype=np.float64)
+    return (eps2 * g + (n + 1.0) * eps1) / (n * eps1 - eps2 * g)
+
+
+def _legendre_all(nmax: int, x: np.ndarray) -> np.ndarray:
+    """P_0..P_nmax at x (Bonnet recurrence)."""
+    P = np.empty((nmax + 1,) + x.shape)
+    P[0] = 1.0
+    if nmax >= 1:
+        P[1] = x
+    for n in range(1, nmax):
+        P[n + 1] = ((2 * n + 1) * x * P[n] - n * P[n - 1]) / (n + 1)
+    return P
+
+
+def kirkwood_energy(charges: np.ndarray, a: float, eps1: float, eps2: float, kappa: float,
+                    center=(0.0, 0.0, 0.0), rtol: float = 1e-13, nmax: int = 400) -> tuple[float, int]:
+    """Kirkwood-series E_sol [kcal/mol] for charges (x,y,z,Q) strictly inside the sphere
+    |y - center| < a.  Terms are added until the last three are below rtol*|E|.
+    Returns (E, number of terms used)."""
+    ch = np.asarray(charges, dtype=np.float64)
+    if ch.shape[0] == 0:
+        return 0.0, 0
+    pos = ch[:, :3] - np.asarray(center)[None, :]
+    Q = ch[:, 3]
+    s = np.linalg.norm(pos, axis=1)
+    if np.any(s >= a):
+        raise ValueError("charges must lie strictly inside the sphere")
+    with np.errstate(invalid="ignore", divide="ignore"):
+        u = np.where(s[:, None] > 0, pos / np.where(s > 0, s, 1.0)[:, None], 0.0)
+    cosg = np.clip(u @ u.T, -1.0, 1.0)
+    f = f_coeff(nmax, eps1, eps2, kappa, a)
+    P = _legendre_all(nmax, cosg)
+    ss = np.outer(s, s) / (a * a)
+    QQ = np.outer(Q, Q)
+    total = 0.0
+    small = 0
+    for n in range(nmax + 1):
+        term = np.sum(QQ * ss ** n * P[n]) * f[n] / (eps1 * a)
+        total += term
+        if n > 2 and abs(term) <= rtol * max(abs(total), 1e-300):
+            small += 1
+            if small >= 3:
+                return 0.5 * C_E * total, n + 1
+        else:
+            small = 0
+    raise RuntimeError("Kirkwood series did not converge within nmax terms")
