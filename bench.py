@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py — FP64 pair-interactions/s and GMRES time-to-solution of the direct-sum BIE-PB
+hot path (Geng & Jacob, arXiv 1301.5885) on 1..8 B200 (one process per GPU).
+
+One STEP = one pass of the whole hot path over the workload:
+bipb_source (Eq. (11)) -> bipb_gmres_solve (GMRES(20), tol 1e-10, one O(N^2) matvec per
+iteration, Eqs. (12)-(13), all-gather across ranks) -> bipb_energy (Eq. (14)), with the
+geometry and charges already resident in HBM (bipb_setup before the timed region).
+value = all pair interactions evaluated by all ranks / max-over-ranks device time.
+e2e   = the same metric through the C ABI with HOST buffers: setup (H2D of geometry +
+charges + x0) + source + solve + energy + D2H of x and E, per step.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bipb_inputs as g  # noqa: E402
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 TFLOP/s at 1965 MHz
+F_REF = 111.0  # FP64 FLOPs per matvec pair of the straightforward libdevice kernel (tools/fref_probe)
+METRIC = "fp64_pair_interactions_per_sec"
+UNIT = "pair-interactions/s"
+RESTART_M, TOL, MAX_IT = 20, 1e-10, 500
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.device)], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), float(p[3]), p[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [r for r in rows if r[2] > 150.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(load), "power_w_max": max(r[2] for r in rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(prob, seconds: float, cores: int):
+    """Time the oracle's matvec (Eqs. (12)-(13), plain C, OpenMP over rows) on a bounded row
+    sample of `prob`; returns (pairs/s, description)."""
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    import oracle
+    oracle.build()
+    u = g.random_vector(2 * prob.n, 3)
+    rows = np.linspace(0, prob.n - 1, max(cores, 16)).astype(np.int64)
+    t = time.perf_counter()
+    oracle.matvec_rows(prob, u, rows)
+    rate = rows.size * (prob.n - 1) / (time.perf_counter() - t)
+    nrows = int(max(cores, min(prob.n, rate * seconds / (prob.n - 1))))
+    rows = np.linspace(0, prob.n - 1, nrows).astype(np.int64)
+    t = time.perf_counter()
+    oracle.matvec_rows(prob, u, rows)
+    dt = time.perf_counter() - t
+    pairs = rows.size * (prob.n - 1)
+    return pairs / dt, f"oracle matvec rows: {rows.size} of {prob.n} target rows x {prob.n - 1} sources " \
+                       f"({pairs:.3e} pairs, {dt:.1f} s, {cores} OpenMP threads)", dt, pairs
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    prob = g.config(args.config)
+    cores = os.cpu_count() or 1
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(prob, per_step, cores)
+    vals, dts, desc = [], [], ""
+    for _ in range(args.steps):
+        v, desc, dt, _p = oracle_sample(prob, per_step, cores)
+        vals.append(v)
+        dts.append(dt)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(dts),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded icosphere + uniform charges)",
+            "config": {"workload": prob.name, "n_elements": prob.n, "n_charges": prob.nc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ native (GPU) arm
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1301_5885_b200 as bp
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    prob = g.config(args.config)
+    n, nc = prob.n, prob.nc
+    uid = None
+    if world > 1:
+        obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    dist_arg = (rank, world, uid, local) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    cen, nrm, area, chg = T(prob.centroids), T(prob.normals), T(prob.areas), T(prob.charges)
+    ctx = bp.bipb_setup(cen, nrm, area, chg, prob.eps1, prob.eps2, prob.kappa, dist=dist_arg,
+                        stream=stream.cuda_stream)
+    x = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+    b = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    e_box = []
+
+    def step():
+        bp.bipb_source(ctx, b)
+        x.zero_()
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, RESTART_M, TOL, MAX_IT, check_true=False)
+        e_box.append(bp.bipb_energy(ctx, x))
+        return rep
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        rep = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.timing_enable(True)
+    ctx.timing_reset()
+    reps, per_step_ms = [], []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between steps (inside the region; ~40 us vs seconds per step)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            reps.append(step())
+            s1.record(stream)
+            s1.synchronize()
+            per_step_ms.append(s0.elapsed_time(s1))
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    mv_ms, mv_launches = ctx.timing_get(0)
+    src_ms, _ = ctx.timing_get(1)
+    en_ms, _ = ctx.timing_get(2)
+    _, all_launches = ctx.timing_get(3)
+    ctx.timing_enable(False)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    matvecs = [r["matvecs"] for r in reps]
+    pairs_per_step = [mv * n * (n - 1) + 2 * n * nc for mv in matvecs]
+    value = sum(pairs_per_step) / (total_ms / 1e3)
+    nloc = bp.bipb_partition(n, world, rank)
+    rows_local = nloc[1] - nloc[0]
+    pairs_per_launch = rows_local * (n - 1)
+    avg_launch_ms = mv_ms / max(mv_launches, 1)
+    achieved = F_REF * pairs_per_launch / (avg_launch_ms / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "bipb::pair_kernel<MATVEC> (FP64 pipe)", "flops_per_unit": F_REF,
+                "unit_of_work": "matvec pair-interaction", "units_per_launch": pairs_per_launch,
+                "avg_launch_ms": avg_launch_ms, "launches": mv_launches,
+                "kernel_share_of_step": mv_ms / max(sum(per_step_ms), 1e-9),
+                "peak_note": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (derived; DFMA microbench measured 34.2)"}
+    clocks = clk.summary()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded icosphere + uniform charges, bipb_inputs)",
+            "config": {"workload": prob.name, "n_elements": n, "n_charges": nc, "restart_m": RESTART_M, "tol": TOL,
+                       "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
+                       "parallelism": f"row-shard x{world} + all-gather", "l2": "flushed between steps (256 MiB)"},
+            "time_to_solution_s": total_ms / args.steps / 1e3,
+            "iterations": [r["iterations"] for r in reps], "matvecs": matvecs,
+            "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),
+            "kernel_ms": {"matvec": mv_ms, "source": src_ms, "energy": en_ms, "steps_sum": sum(per_step_ms)},
+            "roofline": roofline, "clocks": clocks}
+
+    # ---- e2e through the public API with HOST buffers (pinned)
+    ke = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 2)
+    if ke > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hc, hn, ha, hq = pin(prob.centroids), pin(prob.normals), pin(prob.areas), pin(prob.charges)
+        hx = torch.zeros(2 * n, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            c2 = bp.bipb_setup(hc, hn, ha, hq, prob.eps1, prob.eps2, prob.kappa, dist=dist_arg)
+            bp.bipb_source(c2)
+            hx.zero_()
+            st, rep = bp.bipb_gmres_solve(c2, hx, None, RESTART_M, TOL, MAX_IT)
+            e = bp.bipb_energy(c2, hx)
+            c2.close()
+            return rep, e
+
+        if world > 1:
+            # the second context needs its own communicator
+            obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            dist_arg = (rank, world, obj[0], local)
+        e2e_step()
+        times, pairs = [], 0
+        for _ in range(ke):
+            if world > 1:
+                obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                dist_arg = (rank, world, obj[0], local)
+                dist.barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            rep, e = e2e_step()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t)
+            pairs += rep["matvecs"] * n * (n - 1) + 2 * n * nc
+        tsum = sum(times)
+        if world > 1:
+            tt = torch.tensor([tsum], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tsum = float(tt.item())
+        line["e2e"] = {"value": pairs / tsum, "unit": UNIT, "h2d_bytes_per_step": 8 * (7 * n + 4 * nc + 2 * n),
+                       "d2h_bytes_per_step": 8 * (2 * n + 1), "ms_per_step": 1e3 * tsum / ke, "steps": ke,
+                       "timer": "host wall clock around synchronous C-ABI calls"}
+    ctx.close()
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        v, desc, _, _ = oracle_sample(prob, args.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

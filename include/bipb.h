@@ -1,0 +1,167 @@
+/*
+ * bipb.h — C ABI of the B200-native direct-sum boundary-integral Poisson-Boltzmann
+ * hot path (Geng & Jacob, arXiv 1301.5885; "P:<line>" = /root/reference/PAPER.md).
+ *
+ * The library (paper_1301_5885_b200/libbipb.so) evaluates, in FP64 on one or more
+ * B200 GPUs (one process per GPU), the three direct sums of the paper's Table 1
+ * and the restarted GMRES that drives the second one:
+ *   bipb_source      b = [S1; S2]                 Eq. (11), P:242-245   (Table 1 step 6)
+ *   bipb_matvec      y = A u                      Eqs. (12)-(13), P:264-269 (step 11)
+ *   bipb_gmres_solve A x = b, GMRES(m), x0 given  P:271-272, P:342-356 (steps 9-16)
+ *   bipb_energy      E_sol = 1/2 sum q_k phi_reac Eq. (14), P:278-286 (steps 18-21)
+ * with the kernels K1..K4 of Eq. (10) built from G0 = 1/(4 pi r) and
+ * Gk = exp(-kappa r)/(4 pi r) (Eq. (5)), flat triangles with centroid
+ * collocation, the singular self term removed.
+ *
+ * Conventions:
+ *   R1  eps = eps2/eps1 (P:247 prints eps1/eps2; Eqs. (8)-(9) require eps2/eps1).
+ *   R2  S1 = (1/eps1) sum_k q_k G0,  S2 = (1/eps1) sum_k q_k dG0/dnu_x.
+ *   R3  q_k = Q_k in units of e_c; E_sol = 1/2 * 4 pi * 332.0716 * sum_k Q_k phi_reac(x_k)
+ *       in kcal/mol.
+ *   Vectors of length 2N are laid out [phi_1..phi_N, dphi/dnu_1..dphi/dnu_N].
+ *
+ * Pointers: every array argument may be a HOST pointer or a DEVICE pointer on the
+ * context's GPU (detected with cudaPointerGetAttributes).  Device pointers avoid
+ * copies.  All calls are ordered on the context's CUDA stream and return after the
+ * work has completed.  A context is not thread-safe.  Errors are returned as status
+ * codes, never as exceptions or aborts; bipb_last_error() gives a message.
+ *
+ * Multi-GPU (one process per GPU): pass a bipb_dist with the same 128-byte NCCL
+ * unique id on every rank (create it with bipb_nccl_unique_id on rank 0 and
+ * broadcast it).  Target rows are sharded (bipb_partition); every rank holds the full
+ * geometry and charges, passes and receives full-length vectors, and runs the same
+ * (replicated, deterministic) GMRES; an NCCL all-gather reassembles each product.
+ */
+#ifndef BIPB_H
+#define BIPB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bipb_ctx bipb_ctx; /* opaque: owns device memory, stream, NCCL comm */
+
+typedef enum {
+  BIPB_OK = 0,
+  BIPB_ERR_ARG = 1,           /* bad argument (n < 1, nc < 0, NULL where required, m < 1, ...) */
+  BIPB_NOT_CONVERGED = 2,     /* GMRES hit max_iters; x and the report are still filled */
+  BIPB_ERR_INPUT = 3,         /* non-finite input, area <= 0, |normal| not 1 within 1e-6 */
+  BIPB_ERR_SINGULAR = 4,      /* a charge within 1e-6 A of a centroid (S1/S2 singular, R11) */
+  BIPB_ERR_CUDA = 5,          /* CUDA runtime error / no device */
+  BIPB_ERR_NCCL = 6,          /* NCCL missing or failed */
+  BIPB_ERR_OOM = 7            /* device allocation failed */
+} bipb_status;
+
+/* Multi-GPU description; pass NULL for a single GPU. */
+typedef struct {
+  int32_t rank, world;       /* 0 <= rank < world */
+  int32_t device;            /* CUDA device ordinal this rank uses (-1: current device) */
+  unsigned char nccl_uid[128];
+} bipb_dist;
+
+/* GMRES report (iterations, restarts, final residual, history). */
+typedef struct {
+  int64_t iterations;        /* Arnoldi steps (= matvecs inside the Krylov cycles) */
+  int64_t restarts;          /* number of warm restarts taken */
+  int64_t matvecs;           /* all products: iterations + restart residuals + true-residual check */
+  int64_t converged;         /* 1 if the relative residual reached tol */
+  double rel_res_est;        /* |g_{k+1}| / ||b|| from the Givens recurrence */
+  double rel_res_true;       /* ||b - A x|| / ||b|| if check_true was set, else -1 */
+  double* history;           /* caller-owned HOST array for rel_res_est per iteration, may be NULL */
+  int64_t history_cap;       /* its capacity */
+  int64_t history_len;       /* entries produced (may exceed history_cap; extra not stored) */
+} bipb_report;
+
+/*
+ * bipb_setup — Table 1 step 4: copy geometry and charges to the GPU.
+ *   n          number of boundary elements N (>= 1)
+ *   centroids  [n][3] row-major (x, y, z) in Angstrom
+ *   normals    [n][3] unit OUTWARD normals
+ *   areas      [n] element areas W_j > 0 (Eqs. (12)-(13) weights)
+ *   nc         number of point charges N_c (>= 0; 0 => b = 0, x = 0, E = 0)
+ *   charges    [nc][4] rows (x, y, z, Q), Q in units of e_c (R3); may be NULL if nc == 0
+ *   eps1, eps2 solute / solvent dielectric constants (> 0); kappa >= 0 in 1/Angstrom
+ *   dist       NULL for one GPU, else the rank/world/NCCL id (see top)
+ *   cuda_stream a cudaStream_t to order all work on, or NULL for a private stream
+ * The caller's arrays are copied; they may be freed on return.  On success *out owns
+ * all device memory until bipb_destroy.
+ * Errors: ERR_ARG, ERR_INPUT, ERR_SINGULAR, ERR_CUDA, ERR_NCCL, ERR_OOM.
+ */
+bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const double* normals,
+                       const double* areas, int64_t nc, const double* charges, double eps1, double eps2,
+                       double kappa, const bipb_dist* dist, void* cuda_stream);
+
+/*
+ * bipb_source — Eq. (11), Table 1 step 6: b_i = S1(x_i), b_{i+N} = S2(x_i)
+ * over all N_c charges (N x N_c pairs).  The result is kept inside the context (it is
+ * the default right-hand side of bipb_gmres_solve) and, if b != NULL, written to b [2n].
+ */
+bipb_status bipb_source(bipb_ctx* ctx, double* b);
+
+/*
+ * bipb_matvec — Eqs. (12)-(13), Table 1 step 11:
+ *   y_i     = 1/2 (1+eps) u_i     - sum_{j != i} W_j [K1(x_i,x_j) u_{j+N} + K2(x_i,x_j) u_j]
+ *   y_{i+N} = 1/2 (1+1/eps) u_{i+N} - sum_{j != i} W_j [K3(x_i,x_j) u_{j+N} + K4(x_i,x_j) u_j]
+ * u, y: [2n] (must not alias).  N(N-1) pair evaluations, matrix-free.
+ */
+bipb_status bipb_matvec(bipb_ctx* ctx, const double* u, double* y);
+
+/*
+ * bipb_gmres_solve — restarted GMRES(m) with modified Gram-Schmidt Arnoldi and Givens
+ * rotations (Saad), warm restart from the current iterate, on
+ * the device; the host reads one 16-byte residual record per iteration.
+ *   b          [2n] right-hand side, or NULL to use the one from the last bipb_source
+ *   x          [2n] in: initial guess x0 (the paper uses 0); out: solution
+ *   restart_m  Krylov dimension m >= 1 (paper: "every 10-20 steps")
+ *   tol        relative residual target ||b - A x|| / ||b|| (> 0)
+ *   max_iters  cap on Arnoldi steps (>= 1)
+ *   check_true if nonzero, one extra product computes rep->rel_res_true
+ *   rep        may be NULL
+ * Returns BIPB_OK when converged, BIPB_NOT_CONVERGED when max_iters was reached (x and
+ * rep filled).  ||b|| = 0 returns x = 0 at once.
+ */
+bipb_status bipb_gmres_solve(bipb_ctx* ctx, const double* b, double* x, int32_t restart_m, double tol,
+                             int32_t max_iters, int32_t check_true, bipb_report* rep);
+
+/*
+ * bipb_energy — Eq. (14), Table 1 steps 18-21:
+ *   phi_reac(x_k) = sum_j W_j [K1(x_k,x_j) x_{j+N} + K2(x_k,x_j) x_j]   (N_c x N pairs)
+ *   E_sol = 1/2 * 4 pi * 332.0716 * sum_k Q_k phi_reac(x_k)  [kcal/mol]   (R3)
+ *   x        [2n] solved surface potential and normal derivative
+ *   e_sol    out: E_sol (host or device double), required
+ *   phi_reac out: [nc] reaction potentials (internal units e_c/A, R3), may be NULL
+ */
+bipb_status bipb_energy(bipb_ctx* ctx, const double* x, double* e_sol, double* phi_reac);
+
+/* Free everything the context owns (NULL is a no-op). */
+void bipb_destroy(bipb_ctx* ctx);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* bipb_last_error(void);
+
+/* Rows [*r0, *r1) of n owned by `rank` of `world` (equal ceil(n/world) blocks; host-only). */
+void bipb_partition(int64_t n, int32_t world, int32_t rank, int64_t* r0, int64_t* r1);
+
+/* Create a fresh NCCL unique id (rank 0) into out[128].  ERR_NCCL if NCCL is unavailable. */
+bipb_status bipb_nccl_unique_id(unsigned char* out);
+
+/*
+ * Instrumentation (bench.py, tests).  `which`: 0 = matvec pair kernel, 1 = source pair
+ * kernel, 2 = energy pair kernel, 3 = all kernels of the library.
+ * bipb_timing_enable(ctx, 1) brackets each pair-kernel launch with CUDA events on the
+ * context stream; bipb_timing_get returns the summed device time (ms) and the launch
+ * count since the last reset (for which == 3 only the launch count is meaningful).
+ */
+bipb_status bipb_timing_enable(bipb_ctx* ctx, int32_t on);
+bipb_status bipb_timing_get(bipb_ctx* ctx, int32_t which, double* total_ms, int64_t* launches);
+bipb_status bipb_timing_reset(bipb_ctx* ctx);
+
+/* Library version string and the compile-time target ("sm_100a"). */
+const char* bipb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIPB_H */

@@ -44,17 +44,6 @@ def f_coeff(nmax: int, eps1: float, eps2: float, kappa: float, a: float) -> np.n
     return (eps2 * g + (n + 1.0) * eps1) / (n * eps1 - eps2 * g)
 
 
-def _legendre_all(nmax: int, x: np.ndarray) -> np.ndarray:
-    """P_0..P_nmax at x (Bonnet recurrence)."""
-    P = np.empty((nmax + 1,) + x.shape)
-    P[0] = 1.0
-    if nmax >= 1:
-        P[1] = x
-    for n in range(1, nmax):
-        P[n + 1] = ((2 * n + 1) * x * P[n] - n * P[n - 1]) / (n + 1)
-    return P
-
-
 def kirkwood_energy(charges: np.ndarray, a: float, eps1: float, eps2: float, kappa: float,
                     center=(0.0, 0.0, 0.0), rtol: float = 1e-13, nmax: int = 400) -> tuple[float, int]:
     """Kirkwood-series E_sol [kcal/mol] for charges (x,y,z,Q) strictly inside the sphere
@@ -72,13 +61,20 @@ def kirkwood_energy(charges: np.ndarray, a: float, eps1: float, eps2: float, kap
         u = np.where(s[:, None] > 0, pos / np.where(s > 0, s, 1.0)[:, None], 0.0)
     cosg = np.clip(u @ u.T, -1.0, 1.0)
     f = f_coeff(nmax, eps1, eps2, kappa, a)
-    P = _legendre_all(nmax, cosg)
     ss = np.outer(s, s) / (a * a)
     QQ = np.outer(Q, Q)
     total = 0.0
     small = 0
+    p_prev, p_cur = None, np.ones_like(cosg)  # P_0; Bonnet recurrence carried along
+    w = QQ.copy()                              # Q_k Q_l (s_k s_l / a^2)^n
     for n in range(nmax + 1):
-        term = np.sum(QQ * ss ** n * P[n]) * f[n] / (eps1 * a)
+        if n == 1:
+            p_prev, p_cur = p_cur, cosg.copy()
+        elif n > 1:
+            p_prev, p_cur = p_cur, ((2 * n - 1) * cosg * p_cur - (n - 1) * p_prev) / n
+        if n > 0:
+            w *= ss
+        term = float(np.sum(w * p_cur)) * f[n] / (eps1 * a)
         total += term
         if n > 2 and abs(term) <= rtol * max(abs(total), 1e-300):
             small += 1

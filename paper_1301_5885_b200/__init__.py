@@ -1,0 +1,240 @@
+"""paper_1301_5885_b200 — B200-native direct-sum boundary-integral Poisson-Boltzmann hot path.
+
+Thin Python binding (argument marshalling only) over the C ABI in include/bipb.h,
+implemented by libbipb.so (hand-written sm_100a CUDA, built in-tree by build.py).
+Every step of the path — source term (Eq. (11)), matvec (Eqs. (12)-(13)), GMRES
+ and solvation energy (Eq. (14)) of Geng & Jacob, arXiv 1301.5885 —
+runs in the library's kernels.  There is no CPU fallback: importing this package fails
+loudly if libbipb.so is missing, and every call raises BipbError on a non-OK status.
+
+Array arguments may be numpy arrays (host) or torch tensors (host or CUDA), float64 and
+C-contiguous.  CUDA tensors are passed by device pointer (no copies).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbipb.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1301_5885_b200/build.py` "
+                      "(or __graft_entry__.build()); there is no fallback path")
+_lib = ctypes.CDLL(LIB_PATH)
+
+OK, ERR_ARG, NOT_CONVERGED, ERR_INPUT, ERR_SINGULAR, ERR_CUDA, ERR_NCCL, ERR_OOM = range(8)
+_NAMES = {0: "OK", 1: "ERR_ARG", 2: "NOT_CONVERGED", 3: "ERR_INPUT", 4: "ERR_SINGULAR", 5: "ERR_CUDA",
+          6: "ERR_NCCL", 7: "ERR_OOM"}
+
+
+class BipbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"bipb {_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_uid", ctypes.c_ubyte * 128)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("restarts", ctypes.c_int64), ("matvecs", ctypes.c_int64),
+                ("converged", ctypes.c_int64), ("rel_res_est", ctypes.c_double),
+                ("rel_res_true", ctypes.c_double), ("history", ctypes.POINTER(ctypes.c_double)),
+                ("history_cap", ctypes.c_int64), ("history_len", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_I64, _I32, _D = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+_SIGS = {
+    "bipb_setup": ([ctypes.POINTER(_P), _I64, _P, _P, _P, _I64, _P, _D, _D, _D, ctypes.POINTER(Dist), _P], ctypes.c_int),
+    "bipb_source": ([_P, _P], ctypes.c_int),
+    "bipb_matvec": ([_P, _P, _P], ctypes.c_int),
+    "bipb_gmres_solve": ([_P, _P, _P, _I32, _D, _I32, _I32, ctypes.POINTER(Report)], ctypes.c_int),
+    "bipb_energy": ([_P, _P, _P, _P], ctypes.c_int),
+    "bipb_destroy": ([_P], None),
+    "bipb_last_error": ([], ctypes.c_char_p),
+    "bipb_partition": ([_I64, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64)], None),
+    "bipb_nccl_unique_id": ([_P], ctypes.c_int),
+    "bipb_timing_enable": ([_P, _I32], ctypes.c_int),
+    "bipb_timing_get": ([_P, _I32, ctypes.POINTER(_D), ctypes.POINTER(_I64)], ctypes.c_int),
+    "bipb_timing_reset": ([_P], ctypes.c_int),
+    "bipb_version": ([], ctypes.c_char_p),
+}
+EXPORTS = tuple(_SIGS)
+for _name, (_a, _r) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes, _f.restype = _a, _r
+
+
+def _check(st: int):
+    if st != OK:
+        raise BipbError(st, _lib.bipb_last_error().decode())
+
+
+def _ptr(a, writable=False):
+    """(pointer, keepalive) for a float64 C-contiguous numpy array or torch tensor."""
+    if a is None:
+        return None, None
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous or (writable and not a.flags.writeable):
+            raise ValueError("arrays must be float64, C-contiguous (and writable for outputs)")
+        return a.ctypes.data, a
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("tensors must be float64 and contiguous")
+        return a.data_ptr(), a
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def version() -> str:
+    return _lib.bipb_version().decode()
+
+
+def bipb_partition(n: int, world: int, rank: int) -> tuple[int, int]:
+    r0, r1 = _I64(), _I64()
+    _lib.bipb_partition(n, world, rank, ctypes.byref(r0), ctypes.byref(r1))
+    return r0.value, r1.value
+
+
+def bipb_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_lib.bipb_nccl_unique_id(ctypes.cast(buf, _P)))
+    return bytes(buf)
+
+
+class Context:
+    """Owns a bipb_ctx (device geometry, charges, buffers, stream, NCCL comm)."""
+
+    def __init__(self, handle, n, nc, keep):
+        self._h = handle
+        self.n, self.nc = n, nc
+        self._keep = keep
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise BipbError(ERR_ARG, "context destroyed")
+        return self._h
+
+    def close(self):
+        if self._h is not None:
+            _lib.bipb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # instrumentation (bench.py) -------------------------------------------------
+    def timing_enable(self, on=True):
+        _check(_lib.bipb_timing_enable(self.handle, int(on)))
+
+    def timing_reset(self):
+        _check(_lib.bipb_timing_reset(self.handle))
+
+    def timing_get(self, which: int) -> tuple[float, int]:
+        ms, cnt = _D(), _I64()
+        _check(_lib.bipb_timing_get(self.handle, which, ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value, cnt.value
+
+
+def bipb_setup(centroids, normals, areas, charges, eps1, eps2, kappa, dist=None, stream=None) -> Context:
+    """Table 1 step 4: geometry [n,3] x2, areas [n], charges [nc,4] (x,y,z,Q).
+    dist: None or (rank, world, uid_bytes[, device]).  stream: None (library stream) or a
+    cudaStream_t handle (int), e.g. torch.cuda.current_stream().cuda_stream."""
+    n = int(centroids.shape[0])
+    nc = int(charges.shape[0]) if charges is not None else 0
+    pc, kc = _ptr(centroids)
+    pn, kn = _ptr(normals)
+    pa, ka = _ptr(areas)
+    pq, kq = _ptr(charges) if nc > 0 else (None, None)
+    d = None
+    if dist is not None:
+        rank, world, uid = dist[0], dist[1], dist[2]
+        dev = dist[3] if len(dist) > 3 else -1
+        d = Dist(rank=rank, world=world, device=dev)
+        ctypes.memmove(d.nccl_uid, bytes(uid), 128)
+    h = _P()
+    st = _lib.bipb_setup(ctypes.byref(h), n, pc, pn, pa, nc, pq, float(eps1), float(eps2), float(kappa),
+                         ctypes.byref(d) if d is not None else None, stream)
+    _check(st)
+    return Context(h, n, nc, (kc, kn, ka, kq))
+
+
+def _out_like(ctx_n2, like):
+    if like is not None:
+        return like
+    return np.empty(ctx_n2)
+
+
+def bipb_source(ctx: Context, b=None):
+    """Eq. (11): b = [S1; S2] (2n).  Returns b (a new numpy array if b is None)."""
+    b = _out_like(2 * ctx.n, b)
+    pb, _ = _ptr(b, writable=True)
+    _check(_lib.bipb_source(ctx.handle, pb))
+    return b
+
+
+def bipb_matvec(ctx: Context, u, y=None):
+    """Eqs. (12)-(13): y = A u (2n)."""
+    y = _out_like(2 * ctx.n, y)
+    pu, _ = _ptr(u)
+    py, _ = _ptr(y, writable=True)
+    _check(_lib.bipb_matvec(ctx.handle, pu, py))
+    return y
+
+
+def bipb_gmres_solve(ctx: Context, x, b=None, restart_m=20, tol=1e-10, max_iters=500, check_true=False,
+                     history_cap=None, raise_on_not_converged=False):
+    """GMRES(m) on the device.  x holds x0 on entry and the solution on
+    return.  Returns (status, report dict)."""
+    px, _ = _ptr(x, writable=True)
+    pb, _ = _ptr(b)
+    cap = max_iters + 1 if history_cap is None else history_cap
+    hist = np.zeros(max(cap, 1))
+    rep = Report(history=hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap=cap)
+    st = _lib.bipb_gmres_solve(ctx.handle, pb, px, int(restart_m), float(tol), int(max_iters), int(check_true),
+                               ctypes.byref(rep))
+    if st not in (OK, NOT_CONVERGED) or (st == NOT_CONVERGED and raise_on_not_converged):
+        _check(st)
+    return st, {"iterations": rep.iterations, "restarts": rep.restarts, "matvecs": rep.matvecs,
+                "converged": bool(rep.converged), "rel_res_est": rep.rel_res_est,
+                "rel_res_true": rep.rel_res_true, "history": hist[:min(rep.history_len, cap)].copy()}
+
+
+def bipb_energy(ctx: Context, x, phi_reac=None) -> float:
+    """Eq. (14): E_sol [kcal/mol]; optionally fills phi_reac [nc]."""
+    px, _ = _ptr(x)
+    e = np.zeros(1)
+    pp, _ = _ptr(phi_reac, writable=True) if phi_reac is not None else (None, None)
+    _check(_lib.bipb_energy(ctx.handle, px, e.ctypes.data, pp))
+    return float(e[0])
+
+
+def bipb_destroy(ctx: Context):
+    ctx.close()
+
+
+def solve(ctx: Context, x=None, restart_m=20, tol=1e-10, max_iters=500, check_true=False):
+    """Table 1 pipeline on the device: source -> GMRES -> energy.  Returns dict."""
+    b = bipb_source(ctx, None if x is None or isinstance(x, np.ndarray) else _zeros_like(x))
+    if x is None:
+        x = np.zeros(2 * ctx.n)
+    st, rep = bipb_gmres_solve(ctx, x, None, restart_m, tol, max_iters, check_true)
+    e = bipb_energy(ctx, x)
+    return {"b": b, "x": x, "status": st, "report": rep, "energy": e}
+
+
+def _zeros_like(t):
+    return t.new_zeros(t.shape)

@@ -1,0 +1,770 @@
+// bipb.cu — the C ABI (include/bipb.h) over the sm_100a kernels: context, device data
+// layout, launch configuration, the device-resident GMRES(m) driver and the NCCL
+// row-sharded exchange.  Paper: Geng & Jacob, arXiv 1301.5885 (Table 1).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bipb.h"
+#include "bipb_kernels.cuh"
+#include "bipb_vec.cuh"
+
+using namespace bipb;
+
+// ----------------------------------------------------------------- configuration
+// One CTA = TPB threads x T targets per thread against one source chunk.
+#ifndef BIPB_MV_TPB
+#define BIPB_MV_TPB 128
+#endif
+#ifndef BIPB_MV_T
+#define BIPB_MV_T 2
+#endif
+#ifndef BIPB_MV_MINB
+#define BIPB_MV_MINB 4
+#endif
+constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
+constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
+constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
+constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
+
+static thread_local std::string g_err;
+static bipb_status fail(bipb_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(e_ == cudaErrorMemoryAllocation ? BIPB_ERR_OOM : BIPB_ERR_CUDA,                 \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                            \
+  } while (0)
+#define CKS(st)                       \
+  do {                                \
+    bipb_status s_ = (st);            \
+    if (s_ != BIPB_OK) return s_;     \
+  } while (0)
+
+// ------------------------------------------------------------ NCCL via dlopen
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    // reuse an already-loaded libnccl (torch's) when there is one
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (api.h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+      api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+// ------------------------------------------------------------------ context
+struct EventPool {
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t used = 0;
+  int64_t launches = 0;
+};
+
+struct bipb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+
+  int64_t n = 0, nc = 0;
+  double eps1 = 1, eps2 = 1, kappa = 0, eps = 1, s = 1;
+  bool screened = false;
+  int64_t r0 = 0, r1 = 0, np = 0;  // element rows of this rank; padded rows per rank
+  int64_t k0 = 0, k1 = 0, kp = 0;  // charges of this rank; padded per rank
+
+  // device data
+  double *ex = nullptr, *ey = nullptr, *ez = nullptr;     // element centroids x s
+  double *enx = nullptr, *eny = nullptr, *enz = nullptr;  // unit normals
+  double* ew = nullptr;                                   // areas
+  double* rec_el = nullptr;                               // [n][8] source records
+  double *qx = nullptr, *qy = nullptr, *qz = nullptr;     // charge positions x s
+  double* q4 = nullptr;                                   // [nc][4] raw charges (x,y,z,Q)
+  double* rec_ch = nullptr;                               // [nc][4] {x s, y s, z s, Q}
+  double* part = nullptr;
+  size_t part_cap = 0;
+  double* b = nullptr;
+  bool have_b = false;
+  double* stage = nullptr;   // [2 np] or [kp]
+  double* gather = nullptr;  // [world][2 np]
+  double *ubuf = nullptr, *ybuf = nullptr, *xbuf = nullptr, *bbuf = nullptr, *tbuf = nullptr;
+  double* phit = nullptr;  // [nc]
+  double* phi = nullptr;   // [nc]
+  // GMRES
+  double* V = nullptr;
+  int m_cap = 0;
+  double *H = nullptr, *cs = nullptr, *sn = nullptr, *g = nullptr, *yk = nullptr;
+  double* scal = nullptr;  // scalars: [0] beta_b^2, [1] beta, [2] hk1sq, [3] hk1, [4] tmp, [5] energy, [6..7] info
+  double* red_part = nullptr;
+  unsigned* red_cnt = nullptr;
+  double* host_info = nullptr;  // pinned [4]
+  int* dflag = nullptr;
+
+  int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
+
+  bool timing = false;
+  EventPool pool[3];
+  int64_t launches_all = 0;
+};
+
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Source chunk length for a pair launch: chosen from GLOBAL sizes only, so a row's sum
+// order (and value) does not depend on the number of ranks.
+static int64_t choose_chunk(int64_t ntgt_global, int64_t nsrc, int tgt_per_cta) {
+  const int64_t tiles = std::max<int64_t>(1, cdiv(ntgt_global, tgt_per_cta));
+  int64_t nchunk = std::max<int64_t>(16, cdiv(WANT_CTAS, tiles));
+  nchunk = std::min<int64_t>(nchunk, std::max<int64_t>(1, cdiv(nsrc, TILE)));
+  int64_t chunk = cdiv(cdiv(nsrc, nchunk), TILE) * TILE;
+  return std::max<int64_t>(chunk, TILE);
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <typename K>
+static void launch_1d_cfg(int64_t work, int& grid, int& block) {
+  block = 256;
+  grid = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(work, block)), 148 * 8);
+}
+
+static bipb_status timed_begin(bipb_ctx* c, int which, cudaEvent_t* stop_out) {
+  *stop_out = nullptr;
+  c->pool[which].launches++;
+  c->launches_all++;
+  if (!c->timing) return BIPB_OK;
+  EventPool& p = c->pool[which];
+  if (p.used + 2 > p.ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      p.ev.push_back(e);
+    }
+  }
+  CK(cudaEventRecord(p.ev[p.used], c->stream));
+  *stop_out = p.ev[p.used + 1];
+  p.used += 2;
+  return BIPB_OK;
+}
+
+template <typename KernelT>
+static bipb_status set_smem(KernelT k, size_t smem) {
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return BIPB_OK;
+}
+
+// pair launches ----------------------------------------------------------------
+template <int MODE, int TPB, int T, int MINB>
+static bipb_status launch_pair(bipb_ctx* c, const PairArgs& a, int64_t nchunk, int which) {
+  if (a.ntgt <= 0) return BIPB_OK;
+  constexpr int REC = (MODE == SOURCE) ? 4 : 8;
+  const size_t smem = sizeof(double) * STAGES * TILE * REC + 8 * STAGES;
+  dim3 grid((unsigned)cdiv(a.ntgt, TPB * T), (unsigned)nchunk);
+  if (grid.y > 65535) return fail(BIPB_ERR_ARG, "too many source chunks");
+  cudaEvent_t stop;
+  CKS(timed_begin(c, which, &stop));
+  if (c->screened) {
+    auto k = pair_kernel<MODE, TPB, T, true, MINB>;
+    CKS(set_smem(k, smem));
+    k<<<grid, TPB, smem, c->stream>>>(a);
+  } else {
+    auto k = pair_kernel<MODE, TPB, T, false, MINB>;
+    CKS(set_smem(k, smem));
+    k<<<grid, TPB, smem, c->stream>>>(a);
+  }
+  CK(cudaGetLastError());
+  if (stop) CK(cudaEventRecord(stop, c->stream));
+  return BIPB_OK;
+}
+
+static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
+  if (doubles <= c->part_cap) return BIPB_OK;
+  if (c->part) cudaFree(c->part);
+  c->part = nullptr;
+  CK(cudaMalloc(&c->part, doubles * sizeof(double)));
+  c->part_cap = doubles;
+  return BIPB_OK;
+}
+
+#define LAUNCH1D(kern, work, ...)                                   \
+  do {                                                              \
+    int g_, b_;                                                     \
+    launch_1d_cfg<int>((work), g_, b_);                             \
+    kern<<<g_, b_, 0, c->stream>>>(__VA_ARGS__);                    \
+    c->launches_all++;                                              \
+    CK(cudaGetLastError());                                         \
+  } while (0)
+
+// exchange: every rank's rows [r0,r1) of the two halves -> full vector on every rank
+static bipb_status allgather_rows(bipb_ctx* c, double* y) {
+  NcclApi& api = nccl();
+  ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)(2 * c->np), ncclFloat64, c->comm, c->stream);
+  if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+  LAUNCH1D(unpack_kernel, c->world * c->np, c->gather, c->n, c->np, c->world, y);
+  return BIPB_OK;
+}
+
+// y = A u (device vectors of length 2n; y must not alias u)
+static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
+  const int64_t n = c->n;
+  LAUNCH1D(prescale_kernel, n, u, c->ew, c->enx, c->eny, c->enz, c->rec_el, n);
+  const int64_t nloc = c->r1 - c->r0;
+  PairArgs a{};
+  a.tx = c->ex + c->r0; a.ty = c->ey + c->r0; a.tz = c->ez + c->r0;
+  a.tnx = c->enx + c->r0; a.tny = c->eny + c->r0; a.tnz = c->enz + c->r0;
+  a.tgt_begin = c->r0; a.ntgt = nloc;
+  a.src = c->rec_el; a.nsrc = n; a.chunk = c->chunk_mv;
+  a.eps = c->eps; a.inveps = 1.0 / c->eps;
+  a.sc1 = c->s; a.sc2 = c->s * c->s; a.sc3 = c->s * c->s * c->s;
+  a.part = c->part;
+  CKS(ensure_part(c, (size_t)(2 * c->nchunk_mv * std::max<int64_t>(nloc, 1))));
+  a.part = c->part;
+  CKS((launch_pair<MATVEC, MV_TPB, MV_T, MV_MINB>(c, a, c->nchunk_mv, 0)));
+  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
+  if (c->world == 1) {
+    LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u, u + n, d1, d2, y, y + n);
+  } else {
+    LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u + c->r0, u + n + c->r0, d1, d2, c->stage,
+             c->stage + c->np);
+    CKS(allgather_rows(c, y));
+  }
+  return BIPB_OK;
+}
+
+// ||v||^2 or <a,b> into *out (device)
+static bipb_status dot_dev(bipb_ctx* c, const double* a, const double* b, int64_t m, double scale, double* out) {
+  dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(a, b, m, scale, c->red_part, c->red_cnt, out);
+  c->launches_all++;
+  CK(cudaGetLastError());
+  return BIPB_OK;
+}
+
+static bipb_status read_scalars(bipb_ctx* c, const double* dsrc, int count, double* host) {
+  CK(cudaMemcpyAsync(c->host_info, dsrc, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  memcpy(host, c->host_info, sizeof(double) * count);
+  return BIPB_OK;
+}
+
+// input vector -> device pointer (copying host data into `scratch`)
+static bipb_status in_vec(bipb_ctx* c, const double* p, int64_t len, double* scratch, const double** out) {
+  if (is_device_ptr(p)) {
+    *out = p;
+    return BIPB_OK;
+  }
+  CK(cudaMemcpyAsync(scratch, p, sizeof(double) * len, cudaMemcpyHostToDevice, c->stream));
+  *out = scratch;
+  return BIPB_OK;
+}
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* bipb_last_error(void) { return g_err.c_str(); }
+
+const char* bipb_version(void) { return "bipb 0.1 (sm_100a, FP64 direct sum, arXiv 1301.5885)"; }
+
+void bipb_partition(int64_t n, int32_t world, int32_t rank, int64_t* r0, int64_t* r1) {
+  if (world < 1) world = 1;
+  const int64_t np = cdiv(std::max<int64_t>(n, 0), world);
+  int64_t a = std::min<int64_t>((int64_t)rank * np, std::max<int64_t>(n, 0));
+  int64_t b = std::min<int64_t>(a + np, std::max<int64_t>(n, 0));
+  if (r0) *r0 = a;
+  if (r1) *r1 = b;
+}
+
+bipb_status bipb_nccl_unique_id(unsigned char* out) {
+  if (!out) return fail(BIPB_ERR_ARG, "out is NULL");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(BIPB_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, api.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return BIPB_OK;
+}
+
+void bipb_destroy(bipb_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  double* bufs[] = {c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->ew, c->rec_el, c->qx, c->qy, c->qz, c->q4,
+                    c->rec_ch, c->part, c->b, c->stage, c->gather, c->ubuf, c->ybuf, c->xbuf, c->bbuf, c->tbuf,
+                    c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  if (c->red_cnt) cudaFree(c->red_cnt);
+  if (c->dflag) cudaFree(c->dflag);
+  if (c->host_info) cudaFreeHost(c->host_info);
+  for (auto& p : c->pool)
+    for (auto e : p.ev) cudaEventDestroy(e);
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, const double* normals,
+                              const double* areas, int64_t nc, const double* charges, double eps1, double eps2,
+                              double kappa, const bipb_dist* dist, void* cuda_stream) {
+  // ---- host-side validation (bipb.h; SURVEY.md §8(b) "Errors")
+  std::vector<double> C(3 * n), Nn(3 * n), W(n), Q(4 * std::max<int64_t>(nc, 0));
+  auto fetch = [&](const double* src, double* dst, size_t cnt) -> bipb_status {
+    if (cnt == 0) return BIPB_OK;
+    if (is_device_ptr(src)) {
+      CK(cudaMemcpy(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      memcpy(dst, src, cnt * sizeof(double));
+    }
+    return BIPB_OK;
+  };
+  if (dist) {
+    if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world) return fail(BIPB_ERR_ARG, "bad rank/world");
+    if (dist->device >= 0) CK(cudaSetDevice(dist->device));
+  }
+  CK(cudaGetDevice(&c->device));
+  CKS(fetch(centroids, C.data(), 3 * n));
+  CKS(fetch(normals, Nn.data(), 3 * n));
+  CKS(fetch(areas, W.data(), n));
+  CKS(fetch(charges, Q.data(), 4 * nc));
+  if (!(eps1 > 0) || !(eps2 > 0) || !(kappa >= 0) || !std::isfinite(eps1) || !std::isfinite(eps2) ||
+      !std::isfinite(kappa))
+    return fail(BIPB_ERR_INPUT, "eps1, eps2 must be > 0 and kappa >= 0, finite");
+  for (int64_t i = 0; i < n; ++i) {
+    const double* x = &C[3 * i];
+    const double* v = &Nn[3 * i];
+    if (!std::isfinite(x[0]) || !std::isfinite(x[1]) || !std::isfinite(x[2]) || !std::isfinite(W[i]) ||
+        !(W[i] > 0))
+      return fail(BIPB_ERR_INPUT, "element " + std::to_string(i) + ": non-finite centroid or area <= 0");
+    const double nn = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (!(std::fabs(nn - 1.0) <= 1e-6))
+      return fail(BIPB_ERR_INPUT, "element " + std::to_string(i) + ": normal is not unit length");
+  }
+  for (int64_t k = 0; k < nc; ++k)
+    for (int d = 0; d < 4; ++d)
+      if (!std::isfinite(Q[4 * k + d])) return fail(BIPB_ERR_INPUT, "charge " + std::to_string(k) + " not finite");
+
+  c->n = n; c->nc = nc; c->eps1 = eps1; c->eps2 = eps2; c->kappa = kappa;
+  c->eps = eps2 / eps1;  // reading R1
+  c->screened = kappa > 0.0;
+  c->s = c->screened ? kappa : 1.0;
+  c->rank = dist ? dist->rank : 0;
+  c->world = dist ? dist->world : 1;
+  bipb_partition(n, c->world, c->rank, &c->r0, &c->r1);
+  c->np = cdiv(n, c->world);
+  bipb_partition(nc, c->world, c->rank, &c->k0, &c->k1);
+  c->kp = cdiv(std::max<int64_t>(nc, 1), c->world);
+
+  if (cuda_stream) {
+    c->stream = (cudaStream_t)cuda_stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+
+  // ---- device layout: SoA elements (scaled), records, charges
+  std::vector<double> sx(n), sy(n), sz(n), nx(n), ny(n), nz(n), rec(8 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    sx[i] = C[3 * i] * c->s; sy[i] = C[3 * i + 1] * c->s; sz[i] = C[3 * i + 2] * c->s;
+    nx[i] = Nn[3 * i]; ny[i] = Nn[3 * i + 1]; nz[i] = Nn[3 * i + 2];
+    rec[8 * i] = sx[i]; rec[8 * i + 1] = sy[i]; rec[8 * i + 2] = sz[i];
+    for (int d = 3; d < 8; ++d) rec[8 * i + d] = 0.0;
+  }
+  const int64_t ncm = std::max<int64_t>(nc, 1);
+  std::vector<double> qxs(ncm, 0.0), qys(ncm, 0.0), qzs(ncm, 0.0), qrec(4 * ncm, 0.0), q4(4 * ncm, 0.0);
+  for (int64_t k = 0; k < nc; ++k) {
+    qxs[k] = Q[4 * k] * c->s; qys[k] = Q[4 * k + 1] * c->s; qzs[k] = Q[4 * k + 2] * c->s;
+    qrec[4 * k] = qxs[k]; qrec[4 * k + 1] = qys[k]; qrec[4 * k + 2] = qzs[k]; qrec[4 * k + 3] = Q[4 * k + 3];
+    for (int d = 0; d < 4; ++d) q4[4 * k + d] = Q[4 * k + d];
+  }
+  auto up = [&](double** d, const std::vector<double>& h) -> bipb_status {
+    CK(cudaMalloc(d, h.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return BIPB_OK;
+  };
+  CKS(up(&c->ex, sx)); CKS(up(&c->ey, sy)); CKS(up(&c->ez, sz));
+  CKS(up(&c->enx, nx)); CKS(up(&c->eny, ny)); CKS(up(&c->enz, nz));
+  CKS(up(&c->ew, W)); CKS(up(&c->rec_el, rec));
+  CKS(up(&c->qx, qxs)); CKS(up(&c->qy, qys)); CKS(up(&c->qz, qzs));
+  CKS(up(&c->rec_ch, qrec)); CKS(up(&c->q4, q4));
+  const int64_t m2 = 2 * n;
+  CK(cudaMalloc(&c->b, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->ubuf, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->ybuf, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->xbuf, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->bbuf, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->tbuf, m2 * sizeof(double)));
+  CK(cudaMalloc(&c->phit, ncm * sizeof(double)));
+  CK(cudaMalloc(&c->phi, ncm * sizeof(double)));
+  CK(cudaMalloc(&c->scal, 16 * sizeof(double)));
+  CK(cudaMalloc(&c->red_part, RED_BLOCKS * sizeof(double)));
+  CK(cudaMalloc(&c->red_cnt, sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->red_cnt, 0, sizeof(unsigned), c->stream));
+  CK(cudaMalloc(&c->dflag, sizeof(int)));
+  CK(cudaMallocHost(&c->host_info, 8 * sizeof(double)));
+  if (c->world > 1) {
+    const int64_t st = std::max<int64_t>(2 * c->np, c->kp);
+    CK(cudaMalloc(&c->stage, st * sizeof(double)));
+    CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
+  }
+
+  // ---- launch geometry (global sizes only => P-invariant sums)
+  c->chunk_mv = choose_chunk(n, n, MV_TPB * MV_T);
+  c->nchunk_mv = cdiv(n, c->chunk_mv);
+  c->chunk_src = choose_chunk(n, std::max<int64_t>(nc, 1), SRC_TPB * SRC_T);
+  c->nchunk_src = cdiv(std::max<int64_t>(nc, 1), c->chunk_src);
+  c->chunk_en = choose_chunk(std::max<int64_t>(nc, 1), n, EN_TPB * EN_T);
+  c->nchunk_en = cdiv(n, c->chunk_en);
+
+  // ---- singular configuration: a charge within 1e-6 A of a centroid (R11)
+  if (nc > 0) {
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
+    std::vector<double> rx(n), ry(n), rz(n);
+    for (int64_t i = 0; i < n; ++i) { rx[i] = C[3 * i]; ry[i] = C[3 * i + 1]; rz[i] = C[3 * i + 2]; }
+    double *drx, *dry, *drz;
+    CKS(up(&drx, rx)); CKS(up(&dry, ry)); CKS(up(&drz, rz));
+    LAUNCH1D(min_dist_kernel, n, drx, dry, drz, n, c->q4, nc, 1e-12, c->dflag);
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(drx); cudaFree(dry); cudaFree(drz);
+    if (flag) return fail(BIPB_ERR_SINGULAR, "a charge lies within 1e-6 A of an element centroid");
+  }
+
+  // ---- NCCL communicator
+  if (c->world > 1) {
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(BIPB_ERR_NCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_uid, 128);
+    ncclResult_t r = api.CommInitRank(&c->comm, c->world, id, c->rank);
+    if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const double* normals,
+                       const double* areas, int64_t nc, const double* charges, double eps1, double eps2,
+                       double kappa, const bipb_dist* dist, void* cuda_stream) {
+  g_err.clear();
+  if (!out) return fail(BIPB_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(BIPB_ERR_ARG, "n must be >= 1");
+  if (nc < 0) return fail(BIPB_ERR_ARG, "nc must be >= 0");
+  if (!centroids || !normals || !areas || (nc > 0 && !charges)) return fail(BIPB_ERR_ARG, "NULL input array");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(BIPB_ERR_CUDA, "no CUDA device");
+  }
+  bipb_ctx* c = new bipb_ctx();
+  bipb_status st = setup_impl(c, n, centroids, normals, areas, nc, charges, eps1, eps2, kappa, dist, cuda_stream);
+  if (st != BIPB_OK) {
+    std::string keep = g_err;
+    bipb_destroy(c);
+    g_err = keep;
+    return st;
+  }
+  *out = c;
+  return BIPB_OK;
+}
+
+bipb_status bipb_source(bipb_ctx* c, double* b) {
+  if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  const int64_t n = c->n;
+  if (c->nc == 0) {
+    CK(cudaMemsetAsync(c->b, 0, 2 * n * sizeof(double), c->stream));
+  } else {
+    const int64_t nloc = c->r1 - c->r0;
+    PairArgs a{};
+    a.tx = c->ex + c->r0; a.ty = c->ey + c->r0; a.tz = c->ez + c->r0;
+    a.tnx = c->enx + c->r0; a.tny = c->eny + c->r0; a.tnz = c->enz + c->r0;
+    a.tgt_begin = c->r0; a.ntgt = nloc;
+    a.src = c->rec_ch; a.nsrc = c->nc; a.chunk = c->chunk_src;
+    a.eps = c->eps; a.inveps = 1.0 / c->eps;
+    a.sc1 = c->s; a.sc2 = c->s * c->s; a.sc3 = a.sc2 * c->s;
+    CKS(ensure_part(c, (size_t)(2 * c->nchunk_src * std::max<int64_t>(nloc, 1))));
+    a.part = c->part;
+    CKS((launch_pair<SOURCE, SRC_TPB, SRC_T, SRC_MINB>(c, a, c->nchunk_src, 1)));
+    const double scale = 1.0 / (FOUR_PI * c->eps1);
+    if (c->world == 1) {
+      LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->b, c->b + n);
+    } else {
+      LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->stage, c->stage + c->np);
+      CKS(allgather_rows(c, c->b));
+    }
+  }
+  c->have_b = true;
+  if (b) {
+    CK(cudaMemcpyAsync(b, c->b, 2 * n * sizeof(double), cudaMemcpyDefault, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
+  if (!c || !u || !y) return fail(BIPB_ERR_ARG, "NULL argument");
+  if (u == y) return fail(BIPB_ERR_ARG, "u and y must not alias");
+  const int64_t m2 = 2 * c->n;
+  const double* ud;
+  CKS(in_vec(c, u, m2, c->ubuf, &ud));
+  const bool ydev = is_device_ptr(y);
+  double* yd = ydev ? y : c->ybuf;
+  if (ydev && yd == ud) return fail(BIPB_ERR_ARG, "u and y must not alias");
+  CKS(matvec_dev(c, ud, yd));
+  if (!ydev) CK(cudaMemcpyAsync(y, yd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+static bipb_status ensure_krylov(bipb_ctx* c, int m) {
+  if (m <= c->m_cap) return BIPB_OK;
+  double* bufs[] = {c->V, c->H, c->cs, c->sn, c->g, c->yk};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  c->V = c->H = c->cs = c->sn = c->g = c->yk = nullptr;
+  c->m_cap = 0;
+  CK(cudaMalloc(&c->V, (size_t)(m + 1) * 2 * c->n * sizeof(double)));
+  CK(cudaMalloc(&c->H, (size_t)(m + 1) * m * sizeof(double)));
+  CK(cudaMalloc(&c->cs, (size_t)m * sizeof(double)));
+  CK(cudaMalloc(&c->sn, (size_t)m * sizeof(double)));
+  CK(cudaMalloc(&c->g, (size_t)(m + 1) * sizeof(double)));
+  CK(cudaMalloc(&c->yk, (size_t)m * sizeof(double)));
+  c->m_cap = m;
+  return BIPB_OK;
+}
+
+bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t restart_m, double tol,
+                             int32_t max_iters, int32_t check_true, bipb_report* rep) {
+  if (!c || !x) return fail(BIPB_ERR_ARG, "NULL argument");
+  if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
+  if (!b && !c->have_b) return fail(BIPB_ERR_ARG, "b is NULL and bipb_source has not been called");
+  const int64_t m2 = 2 * c->n;
+  const int m = restart_m;
+  CKS(ensure_krylov(c, m));
+  const double* bd = c->b;
+  if (b) CKS(in_vec(c, b, m2, c->bbuf, &bd));
+  const bool xdev = is_device_ptr(x);
+  double* xd = xdev ? x : c->xbuf;
+  if (!xdev) CK(cudaMemcpyAsync(xd, x, m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  double* S = c->scal;  // [0] ||b||, [1] beta, [2] hk1sq, [3] hk1, [4] ||x||^2
+  int64_t its = 0, restarts = 0, matvecs = 0, hl = 0;
+  bool converged = false;
+  double rel = 1.0, h2[2];
+  if (rep) rep->rel_res_true = -1.0;
+
+  CKS(dot_dev(c, bd, bd, m2, 1.0, S + 0));
+  LAUNCH1D(sqrt_kernel, 1, S + 0, S + 0);
+  CKS(read_scalars(c, S, 1, h2));
+  const double beta_b = h2[0];
+  if (beta_b == 0.0) {
+    CK(cudaMemsetAsync(xd, 0, m2 * sizeof(double), c->stream));
+    converged = true;
+    rel = 0.0;
+    if (rep) rep->rel_res_true = 0.0;
+  } else {
+    bool first = true;
+    for (;;) {
+      // r = b - A x  (x = 0 => r = b without a product), into V[0]
+      CKS(dot_dev(c, xd, xd, m2, 1.0, S + 4));
+      CKS(read_scalars(c, S + 4, 1, h2));
+      if (h2[0] == 0.0) {
+        CK(cudaMemcpyAsync(c->V, bd, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      } else {
+        CKS(matvec_dev(c, xd, c->tbuf));
+        ++matvecs;
+        LAUNCH1D(residual_kernel, m2, c->V, bd, c->tbuf, m2);
+      }
+      if (!first) ++restarts;
+      first = false;
+      CKS(dot_dev(c, c->V, c->V, m2, 1.0, S + 1));
+      LAUNCH1D(sqrt_kernel, 1, S + 1, S + 1);
+      CKS(read_scalars(c, S + 1, 1, h2));
+      rel = h2[0] / beta_b;
+      if (rel <= tol) { converged = true; break; }
+      if (its >= max_iters) break;
+      LAUNCH1D(scale_div_kernel, m2, c->V, c->V, S + 1, m2);
+      init_g_kernel<<<1, 32, 0, c->stream>>>(c->g, S + 1, m);
+      c->launches_all++;
+      int kdone = 0;
+      for (int k = 0; k < m; ++k) {
+        double* vk = c->V + (int64_t)k * m2;
+        double* w = c->V + (int64_t)(k + 1) * m2;
+        CKS(matvec_dev(c, vk, w));
+        ++matvecs;
+        ++its;
+        // modified Gram-Schmidt: h_ik = <w, v_i>; w -= h_ik v_i  (i = 0..k), then ||w||^2
+        axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, nullptr, nullptr, c->V, m2, c->red_part,
+                                                                    c->red_cnt, c->H + 0 * m + k);
+        c->launches_all++;
+        for (int i = 0; i <= k; ++i) {
+          const double* zi = (i < k) ? c->V + (int64_t)(i + 1) * m2 : w;
+          double* outp = (i < k) ? c->H + (int64_t)(i + 1) * m + k : S + 2;
+          axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, c->V + (int64_t)i * m2, c->H + (int64_t)i * m + k,
+                                                                      zi, m2, c->red_part, c->red_cnt, outp);
+          c->launches_all++;
+        }
+        CK(cudaGetLastError());
+        givens_kernel<<<1, 1, 0, c->stream>>>(c->H, c->cs, c->sn, c->g, S + 2, S + 3, k, m, beta_b, S + 6);
+        c->launches_all++;
+        CKS(read_scalars(c, S + 6, 2, h2));
+        rel = h2[0];
+        const double hk1 = h2[1];
+        if (rep && rep->history && hl < rep->history_cap) rep->history[hl] = rel;
+        ++hl;
+        kdone = k + 1;
+        if (hk1 <= 1e-14 * beta_b) break;  // happy breakdown
+        LAUNCH1D(scale_div_kernel, m2, w, w, S + 3, m2);
+        if (rel <= tol || its >= max_iters) break;
+      }
+      backsolve_kernel<<<1, 1, 0, c->stream>>>(c->H, c->g, c->yk, kdone, m);
+      c->launches_all++;
+      LAUNCH1D(update_x_kernel, m2, xd, c->V, c->yk, kdone, m2);
+      if (rel <= tol) { converged = true; break; }
+      if (its >= max_iters) break;
+    }
+    if (check_true) {
+      CKS(matvec_dev(c, xd, c->tbuf));
+      ++matvecs;
+      LAUNCH1D(residual_kernel, m2, c->tbuf, bd, c->tbuf, m2);
+      CKS(dot_dev(c, c->tbuf, c->tbuf, m2, 1.0, S + 4));
+      LAUNCH1D(sqrt_kernel, 1, S + 4, S + 4);
+      CKS(read_scalars(c, S + 4, 1, h2));
+      if (rep) rep->rel_res_true = h2[0] / beta_b;
+    }
+  }
+  if (!xdev) CK(cudaMemcpyAsync(x, xd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (rep) {
+    rep->iterations = its;
+    rep->restarts = restarts;
+    rep->matvecs = matvecs;
+    rep->converged = converged ? 1 : 0;
+    rep->rel_res_est = rel;
+    rep->history_len = hl;
+  }
+  if (!converged) return fail(BIPB_NOT_CONVERGED, "GMRES reached max_iters");
+  return BIPB_OK;
+}
+
+bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi_reac) {
+  if (!c || !x || !e_sol) return fail(BIPB_ERR_ARG, "NULL argument");
+  const int64_t n = c->n, nc = c->nc, m2 = 2 * n;
+  double e = 0.0;
+  if (nc > 0) {
+    const double* xd;
+    CKS(in_vec(c, x, m2, c->ubuf, &xd));
+    LAUNCH1D(prescale_kernel, n, xd, c->ew, c->enx, c->eny, c->enz, c->rec_el, n);
+    const int64_t kloc = c->k1 - c->k0;
+    PairArgs a{};
+    a.tx = c->qx + c->k0; a.ty = c->qy + c->k0; a.tz = c->qz + c->k0;
+    a.tgt_begin = c->k0; a.ntgt = kloc;
+    a.src = c->rec_el; a.nsrc = n; a.chunk = c->chunk_en;
+    a.eps = c->eps; a.inveps = 1.0 / c->eps;
+    a.sc1 = c->s; a.sc2 = c->s * c->s; a.sc3 = a.sc2 * c->s;
+    CKS(ensure_part(c, (size_t)(2 * c->nchunk_en * std::max<int64_t>(kloc, 1))));
+    a.part = c->part;
+    CKS((launch_pair<ENERGY, EN_TPB, EN_T, EN_MINB>(c, a, c->nchunk_en, 2)));
+    if (c->world == 1) {
+      LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->phit);
+    } else {
+      LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->stage);
+      NcclApi& api = nccl();
+      ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)c->kp, ncclFloat64, c->comm, c->stream);
+      if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+      LAUNCH1D(unpack1_kernel, c->world * c->kp, c->gather, nc, c->kp, c->world, c->phit);
+    }
+    energy_sum_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(c->q4, c->phit, nc, c->red_part, c->red_cnt,
+                                                                  c->scal + 5);
+    c->launches_all++;
+    CK(cudaGetLastError());
+    double h[1];
+    CKS(read_scalars(c, c->scal + 5, 1, h));
+    e = h[0];
+    if (phi_reac) {
+      LAUNCH1D(phi_scale_kernel, nc, c->phit, c->phi, nc);
+      CK(cudaMemcpyAsync(phi_reac, c->phi, nc * sizeof(double), cudaMemcpyDefault, c->stream));
+    }
+  }
+  CK(cudaMemcpyAsync(e_sol, &e, sizeof(double), cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+bipb_status bipb_timing_enable(bipb_ctx* c, int32_t on) {
+  if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  c->timing = on != 0;
+  return BIPB_OK;
+}
+
+bipb_status bipb_timing_reset(bipb_ctx* c) {
+  if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& p : c->pool) {
+    p.used = 0;
+    p.launches = 0;
+  }
+  c->launches_all = 0;
+  return BIPB_OK;
+}
+
+bipb_status bipb_timing_get(bipb_ctx* c, int32_t which, double* total_ms, int64_t* launches) {
+  if (!c || which < 0 || which > 3) return fail(BIPB_ERR_ARG, "bad argument");
+  CK(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  int64_t cnt = 0;
+  if (which == 3) {
+    cnt = c->launches_all;
+  } else {
+    EventPool& p = c->pool[which];
+    for (size_t i = 0; i + 1 < p.used; i += 2) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, p.ev[i], p.ev[i + 1]));
+      tot += ms;
+    }
+    cnt = p.launches;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = cnt;
+  return BIPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+"""Write tests/golden/oracle_<cfg>.json: full oracle solves (source -> GMRES -> energy) of
+BASELINE configs, keyed by the input SHA-256.  Calls ONLY oracle/ and bipb_inputs/
+(never the CUDA path).  Usage: python tests/make_oracle_golden.py C1 C2 [C3 ...]"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
+
+import bipb_inputs as g  # noqa: E402
+import oracle  # noqa: E402
+
+
+def main(names, restarts=(20,)):
+    for name in names:
+        p = g.config(name)
+        out = {"config": name, "sha256": p.sha256(), "n": p.n, "nc": p.nc, "eps1": p.eps1, "eps2": p.eps2,
+               "kappa": p.kappa, "tol": 1e-10, "solves": {}}
+        rows = np.unique(np.linspace(0, p.n - 1, 64).astype(np.int64))
+        for m in restarts:
+            t = time.time()
+            r = oracle.solve(p, restart=m, tol=1e-10, max_iters=500, check_true=True)
+            out["solves"][str(m)] = {
+                "energy": r["energy"], "status": r["status"], "iterations": r["report"]["iterations"],
+                "restarts": r["report"]["restarts"], "matvecs": r["report"]["matvecs"],
+                "rel_res_true": r["report"]["rel_res_true"], "seconds": time.time() - t,
+                "rows": rows.tolist(), "x_phi": r["x"][rows].tolist(), "x_dphi": r["x"][rows + p.n].tolist(),
+                "b_phi": r["b"][rows].tolist(), "b_dphi": r["b"][rows + p.n].tolist(),
+                "b_norm": float(np.linalg.norm(r["b"])), "x_norm": float(np.linalg.norm(r["x"]))}
+            print(name, m, out["solves"][str(m)]["energy"], out["solves"][str(m)]["iterations"],
+                  f"{time.time() - t:.1f}s", flush=True)
+        with open(os.path.join(ROOT, "tests", "golden", f"oracle_{name}.json"), "w") as f:
+            json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:] or ["C1", "C2"]
+    ms = (10, 20) if all(a in ("C1", "C2") for a in args) else (20,)
+    main(args, ms)

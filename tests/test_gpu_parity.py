@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI, via the thin binding) against the CPU oracle
+on the same seeded inputs.  Tolerances are north_star's (BASELINE.json): matvec rel-L2 <= 1e-11
+(overall and per block), source <= 1e-12, energy <= 1e-8 relative at GMRES tol 1e-10,
+iterations within +-1."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import bipb_inputs as g
+import oracle
+from oracle.kirkwood import kirkwood_energy
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def bp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1301_5885_b200 as bp
+    return bp
+
+
+def _ctx(bp, p):
+    return bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _ragged(L, R, keep, seed, charges, kappa=g.KAPPA):
+    """Icosphere with a random subset of elements kept (N not a multiple of any tile)."""
+    p = g.sphere_problem(L, R, charges, kappa=kappa)
+    idx = np.sort(np.random.default_rng(seed).choice(p.n, keep, replace=False))
+    return g.Problem(f"ragged{keep}", np.ascontiguousarray(p.centroids[idx]), np.ascontiguousarray(p.normals[idx]),
+                     np.ascontiguousarray(p.areas[idx]), p.charges, p.eps1, p.eps2, kappa)
+
+
+CASES = [
+    ("L2", lambda k: g.sphere_problem(2, 4.0, g.helix_charges(), kappa=k)),
+    ("L3", lambda k: g.sphere_problem(3, 4.0, g.charges_in_ball(20, 3.0, 7), kappa=k)),
+    ("C1", lambda k: g.sphere_problem(4, 2.0, np.array([[0.0, 0, 0, 1.0]]), kappa=k)),
+    ("ragged4999", lambda k: _ragged(4, 4.0, 4999, 1, g.charges_in_ball(37, 3.0, 8), k)),
+    ("ellipsoidL4", lambda k: g.Problem("ell", *g.elements(*g.ellipsoid(4, (24.0, 18.0, 14.0))),
+                                       g.charges_in_ball(300, 1.0, 3, axes=(21.0, 15.0, 11.0)), kappa=k)),
+]
+
+
+@pytest.mark.parametrize("kappa", [g.KAPPA, 0.0])
+@pytest.mark.parametrize("name,make", CASES)
+def test_matvec_parity(bp, name, make, kappa):
+    p = make(kappa)
+    ctx = _ctx(bp, p)
+    for u in (g.random_vector(2 * p.n, 11), g.random_vector(2 * p.n, 0, smooth_centroids=p.centroids)):
+        y = bp.bipb_matvec(ctx, u)
+        ref = oracle.matvec(p, u)
+        n = p.n
+        assert _rel(y, ref) <= 1e-11
+        assert _rel(y[:n], ref[:n]) <= 1e-11 and _rel(y[n:], ref[n:]) <= 1e-11
+        # element-wise (relative to the row scale of each block)
+        assert np.max(np.abs(y[:n] - ref[:n])) <= 1e-11 * np.max(np.abs(ref[:n]))
+        assert np.max(np.abs(y[n:] - ref[n:])) <= 1e-11 * np.max(np.abs(ref[n:]))
+    ctx.close()
+
+
+@pytest.mark.parametrize("name,make", CASES)
+def test_source_and_energy_parity(bp, name, make):
+    p = make(g.KAPPA)
+    ctx = _ctx(bp, p)
+    b = bp.bipb_source(ctx)
+    bo = oracle.source(p)
+    assert _rel(b[:p.n], bo[:p.n]) <= 1e-12 and _rel(b[p.n:], bo[p.n:]) <= 1e-12
+    x = g.random_vector(2 * p.n, 5)
+    phi = np.zeros(p.nc)
+    e = bp.bipb_energy(ctx, x, phi)
+    phio = oracle.reaction_potential(p, x)
+    assert _rel(phi, phio) <= 1e-12
+    assert e == pytest.approx(oracle.energy(p, x), rel=1e-11)
+    ctx.close()
+
+
+@pytest.mark.parametrize("m", [10, 20])
+@pytest.mark.parametrize("name,make", CASES[:4])
+def test_solve_parity_small(bp, name, make, m):
+    p = make(g.KAPPA)
+    ref = oracle.solve(p, restart=m, tol=1e-10)
+    ctx = _ctx(bp, p)
+    x = np.zeros(2 * p.n)
+    bp.bipb_source(ctx)
+    st, rep = bp.bipb_gmres_solve(ctx, x, None, m, 1e-10, 500, check_true=True)
+    e = bp.bipb_energy(ctx, x)
+    assert st == bp.OK and rep["converged"]
+    assert abs(rep["iterations"] - ref["report"]["iterations"]) <= 1
+    assert e == pytest.approx(ref["energy"], rel=1e-8)
+    assert rep["rel_res_true"] <= 1e-9
+    assert _rel(x, ref["x"]) <= 1e-8
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_solve_parity_golden(bp, cfg):
+    """Full-size BASELINE configs against stored oracle solves (tests/make_oracle_golden.py)."""
+    path = os.path.join(GOLD, f"oracle_{cfg}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    gold = json.load(open(path))
+    p = g.config(cfg)
+    assert p.sha256() == gold["sha256"]
+    ctx = _ctx(bp, p)
+    b = bp.bipb_source(ctx)
+    for m, ref in gold["solves"].items():
+        rows = np.array(ref["rows"])
+        np.testing.assert_allclose(b[rows], ref["b_phi"], rtol=1e-12, atol=1e-14 * ref["b_norm"])
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, int(m), gold["tol"], 500, check_true=True)
+        e = bp.bipb_energy(ctx, x)
+        assert st == bp.OK
+        assert abs(rep["iterations"] - ref["iterations"]) <= 1
+        assert e == pytest.approx(ref["energy"], rel=1e-8)
+        np.testing.assert_allclose(x[rows], ref["x_phi"], rtol=1e-7, atol=1e-9 * ref["x_norm"])
+    ctx.close()
+
+
+def test_full_size_c4_sampled(bp):
+    """C4 (N = 327,680, the bench workload): sampled rows of the matvec and source, sampled
+    charges of phi_reac against the oracle; the solved energy against the Kirkwood series
+    (a property that holds at any size: BEM -> Kirkwood with discretisation error ~1e-3)."""
+    p = g.config("C4")
+    ctx = _ctx(bp, p)
+    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 24).astype(np.int64), [0, 1, 255, 256, p.n - 1]]))
+    u = g.random_vector(2 * p.n, 21)
+    y = bp.bipb_matvec(ctx, u)
+    yi, yin = oracle.matvec_rows(p, u, rows)
+    assert np.max(np.abs(y[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
+    assert np.max(np.abs(y[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))
+    b = bp.bipb_source(ctx)
+    sub = g.Problem("sub", p.centroids[rows], p.normals[rows], p.areas[rows], p.charges, p.eps1, p.eps2, p.kappa)
+    bo = oracle.source(sub)
+    np.testing.assert_allclose(b[rows], bo[:rows.size], rtol=1e-12)
+    np.testing.assert_allclose(b[rows + p.n], bo[rows.size:], rtol=1e-10, atol=1e-13 * np.abs(bo[rows.size:]).max())
+    ks = np.linspace(0, p.nc - 1, 16).astype(np.int64)
+    phi = np.zeros(p.nc)
+    bp.bipb_energy(ctx, u, phi)
+    subq = g.Problem("subq", p.centroids, p.normals, p.areas, np.ascontiguousarray(p.charges[ks]), p.eps1, p.eps2,
+                     p.kappa)
+    np.testing.assert_allclose(phi[ks], oracle.reaction_potential(subq, u), rtol=1e-11,
+                               atol=1e-13 * np.abs(phi).max())
+    x = np.zeros(2 * p.n)
+    st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 500, check_true=True)
+    e = bp.bipb_energy(ctx, x)
+    kpath = os.path.join(GOLD, "kirkwood.json")
+    ek = json.load(open(kpath))["C4"]["energy"] if os.path.exists(kpath) else \
+        kirkwood_energy(p.charges, 20.0, p.eps1, p.eps2, p.kappa)[0]
+    assert st == bp.OK and rep["rel_res_true"] <= 1e-9
+    assert abs(e / ek - 1) < 5e-3
+    assert 10 <= rep["iterations"] <= 60
+    ctx.close()
+
+
+def test_degenerate_and_errors(bp):
+    # N = 1: sums are empty -> y = (1/2 (1+eps) u1, 1/2 (1+1/eps) u2)
+    p = g.Problem("n1", np.array([[1.0, 0, 0]]), np.array([[1.0, 0, 0]]), np.array([0.3]), np.zeros((0, 4)))
+    ctx = _ctx(bp, p)
+    y = bp.bipb_matvec(ctx, np.array([2.0, 3.0]))
+    assert y[0] == 0.5 * 81.0 * 2.0 and y[1] == pytest.approx(0.5 * (1 + 1 / 80.0) * 3.0, rel=1e-15)
+    # N_c = 0: b = 0, x = 0, E = 0 (R17)
+    b = bp.bipb_source(ctx)
+    assert np.all(b == 0)
+    x = np.ones(2)
+    st, rep = bp.bipb_gmres_solve(ctx, x)
+    assert st == bp.OK and np.all(x == 0) and rep["iterations"] == 0
+    assert bp.bipb_energy(ctx, x) == 0.0
+    ctx.close()
+    # N = 2 against the oracle
+    q = g.Problem("n2", np.array([[1.0, 0, 0], [0.0, 1.3, 0.2]]), np.array([[1.0, 0, 0], [0, 1.0, 0]]),
+                  np.array([0.3, 0.2]), np.array([[0.1, 0.1, 0.1, 1.0]]))
+    ctx = _ctx(bp, q)
+    u = np.array([0.3, -1.0, 2.0, 0.7])
+    assert _rel(bp.bipb_matvec(ctx, u), oracle.matvec(q, u)) <= 1e-14
+    ctx.close()
+    c1 = g.config("C1")
+    bad = c1.areas.copy()
+    bad[3] = 0.0
+    with pytest.raises(bp.BipbError) as ei:
+        bp.bipb_setup(c1.centroids, c1.normals, bad, c1.charges, 1, 80, 0.1)
+    assert ei.value.status == bp.ERR_INPUT
+    nb = c1.normals.copy()
+    nb[0] *= 1.01
+    with pytest.raises(bp.BipbError) as ei:
+        bp.bipb_setup(c1.centroids, nb, c1.areas, c1.charges, 1, 80, 0.1)
+    assert ei.value.status == bp.ERR_INPUT
+    ch = np.array([[*c1.centroids[17], 1.0]])
+    with pytest.raises(bp.BipbError) as ei:
+        bp.bipb_setup(c1.centroids, c1.normals, c1.areas, ch, 1, 80, 0.1)
+    assert ei.value.status == bp.ERR_SINGULAR
+    # max_iters reached -> NOT_CONVERGED with x filled
+    ctx = _ctx(bp, c1)
+    bp.bipb_source(ctx)
+    x = np.zeros(2 * c1.n)
+    st, rep = bp.bipb_gmres_solve(ctx, x, None, 5, 1e-14, 7)
+    assert st == bp.NOT_CONVERGED and rep["iterations"] == 7 and np.linalg.norm(x) > 0
+    ctx.close()
+
+
+def test_device_pointers_and_determinism(bp):
+    import torch
+    p = g.sphere_problem(3, 4.0, g.helix_charges())
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = bp.bipb_setup(T(p.centroids), T(p.normals), T(p.areas), T(p.charges), 1.0, 80.0, g.KAPPA,
+                        stream=torch.cuda.current_stream().cuda_stream)
+    u = T(g.random_vector(2 * p.n, 3))
+    y1 = torch.empty_like(u)
+    y2 = torch.empty_like(u)
+    bp.bipb_matvec(ctx, u, y1)
+    bp.bipb_matvec(ctx, u, y2)
+    assert torch.equal(y1, y2)  # bitwise reproducible
+    ref = oracle.matvec(p, u.cpu().numpy())
+    assert _rel(y1.cpu().numpy(), ref) <= 1e-11
+    x = torch.zeros(2 * p.n, dtype=torch.float64, device=dev)
+    bp.bipb_source(ctx)
+    st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 200)
+    x2 = torch.zeros_like(x)
+    st2, rep2 = bp.bipb_gmres_solve(ctx, x2, None, 20, 1e-10, 200)
+    assert torch.equal(x, x2) and rep["iterations"] == rep2["iterations"]
+    ctx.close()
