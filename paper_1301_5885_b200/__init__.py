@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbipb.so")
+LIB_PATH = os.environ.get("BIPB_LIB") or os.path.join(_HERE, "libbipb.so")  # BIPB_LIB: tuning variants only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1301_5885_b200/build.py` "

@@ -23,10 +23,10 @@ using namespace bipb;
 #define BIPB_MV_TPB 128
 #endif
 #ifndef BIPB_MV_T
-#define BIPB_MV_T 2
+#define BIPB_MV_T 3
 #endif
 #ifndef BIPB_MV_MINB
-#define BIPB_MV_MINB 4
+#define BIPB_MV_MINB 3
 #endif
 constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
@@ -144,7 +144,7 @@ static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // order (and value) does not depend on the number of ranks.
 static int64_t choose_chunk(int64_t ntgt_global, int64_t nsrc, int tgt_per_cta) {
   const int64_t tiles = std::max<int64_t>(1, cdiv(ntgt_global, tgt_per_cta));
-  int64_t nchunk = std::max<int64_t>(16, cdiv(WANT_CTAS, tiles));
+  int64_t nchunk = std::max<int64_t>(32, cdiv(WANT_CTAS, tiles));
   nchunk = std::min<int64_t>(nchunk, std::max<int64_t>(1, cdiv(nsrc, TILE)));
   int64_t chunk = cdiv(cdiv(nsrc, nchunk), TILE) * TILE;
   return std::max<int64_t>(chunk, TILE);
@@ -381,6 +381,11 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     for (int d = 0; d < 4; ++d)
       if (!std::isfinite(Q[4 * k + d])) return fail(BIPB_ERR_INPUT, "charge " + std::to_string(k) + " not finite");
 
+  {  // exp table T[j] = 2^(-j/2^B), correctly rounded on the host (long double)
+    double tab[EXP_TAB];
+    for (int j = 0; j < EXP_TAB; ++j) tab[j] = (double)exp2l(-(long double)j / EXP_TAB);
+    CK(cudaMemcpyToSymbol(c_exp_tab, tab, sizeof(tab)));
+  }
   c->n = n; c->nc = nc; c->eps1 = eps1; c->eps2 = eps2; c->kappa = kappa;
   c->eps = eps2 / eps1;  // reading R1
   c->screened = kappa > 0.0;

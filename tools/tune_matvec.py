@@ -1,0 +1,88 @@
+"""Build (here) or time (on the GPU) launch-configuration variants of the matvec pair kernel.
+  python tools/tune_matvec.py build            # nvcc all variants into build/variants/
+  python tools/tune_matvec.py run [C4] [reps]  # time each variant in a subprocess
+"""
+import itertools
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "variants")
+
+VARIANTS = []
+for tpb, t, minb, eb in [(128, 2, 4, 8), (128, 3, 3, 8), (128, 4, 2, 8), (64, 4, 4, 8), (64, 3, 6, 8),
+                         (128, 4, 2, 6), (256, 2, 2, 8), (64, 2, 8, 8), (128, 1, 8, 8)]:
+    VARIANTS.append({"tpb": tpb, "t": t, "minb": minb, "exp_bits": eb})
+
+
+def name(v):
+    return f"tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}"
+
+
+def build():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("b", os.path.join(ROOT, "paper_1301_5885_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    os.makedirs(OUT, exist_ok=True)
+    procs = []
+    for v in VARIANTS:
+        extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
+                 f"-DBIPB_EXP_BITS={v['exp_bits']}"]
+        out = os.path.join(OUT, f"libbipb_{name(v)}.so")
+        cmd = [b.NVCC, *b.FLAGS, *extra, "-o", out, *b.SRC, "-ldl"]
+        procs.append(subprocess.Popen(cmd))
+    for p in procs:
+        assert p.wait() == 0
+
+
+def one(cfg, reps):
+    import numpy as np
+    import torch
+    import bipb_inputs as g
+    import paper_1301_5885_b200 as bp
+    p = g.config(cfg)
+    ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa)
+    dev = torch.device("cuda:0")
+    u = torch.from_numpy(g.random_vector(2 * p.n, 1)).to(dev)
+    y = torch.empty_like(u)
+    bp.bipb_matvec(ctx, u, y)
+    ctx.timing_enable(True)
+    ctx.timing_reset()
+    for _ in range(reps):
+        bp.bipb_matvec(ctx, u, y)
+    ms, cnt = ctx.timing_get(0)
+    ctx.close()
+    per = ms / cnt
+    return {"ms": per, "pairs_per_s": p.n * (p.n - 1) / (per / 1e3), "checksum": float(y.norm().item()),
+            "y0": float(y[0].item())}
+
+
+def run(cfg, reps):
+    res = []
+    for v in VARIANTS:
+        lib = os.path.join(OUT, f"libbipb_{name(v)}.so")
+        env = dict(os.environ, BIPB_LIB=lib)
+        out = subprocess.run([sys.executable, __file__, "one", cfg, str(reps)], env=env, capture_output=True,
+                             text=True, timeout=600)
+        try:
+            r = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception:
+            r = {"error": out.stderr[-500:]}
+        r.update(v)
+        res.append(r)
+        print(json.dumps(r), flush=True)
+    return res
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1]
+    if cmd == "build":
+        build()
+    elif cmd == "one":
+        print(json.dumps(one(sys.argv[2], int(sys.argv[3]))))
+    else:
+        run(sys.argv[2] if len(sys.argv) > 2 else "C4", int(sys.argv[3]) if len(sys.argv) > 3 else 3)
