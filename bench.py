@@ -171,11 +171,8 @@ def run_native(args):
         dist.init_process_group("nccl", device_id=dev)
     prob = g.config(args.config)
     n, nc = prob.n, prob.nc
-    uid = None
-    if world > 1:
-        obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+    from paper_1301_5885_b200 import dist as bd
+    uid = bd.share_uid(bp.bipb_nccl_unique_id, rank, world)
     dist_arg = (rank, world, uid, local) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -229,10 +226,7 @@ def run_native(args):
     en_ms, _ = ctx.timing_get(2)
     _, all_launches = ctx.timing_get(3)
     ctx.timing_enable(False)
-    if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    total_ms = bd.max_over_ranks(total_ms, world, dev)
     matvecs = [r["matvecs"] for r in reps]
     pairs_per_step = [mv * n * (n - 1) + 2 * n * nc for mv in matvecs]
     value = sum(pairs_per_step) / (total_ms / 1e3)
@@ -278,18 +272,13 @@ def run_native(args):
             c2.close()
             return rep, e
 
-        if world > 1:
-            # the second context needs its own communicator
-            obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            dist_arg = (rank, world, obj[0], local)
+        if world > 1:  # every context owns its own communicator
+            dist_arg = (rank, world, bd.share_uid(bp.bipb_nccl_unique_id, rank, world), local)
         e2e_step()
         times, pairs = [], 0
         for _ in range(ke):
             if world > 1:
-                obj = [bp.bipb_nccl_unique_id() if rank == 0 else None]
-                dist.broadcast_object_list(obj, src=0)
-                dist_arg = (rank, world, obj[0], local)
+                dist_arg = (rank, world, bd.share_uid(bp.bipb_nccl_unique_id, rank, world), local)
                 dist.barrier()
             torch.cuda.synchronize()
             t = time.perf_counter()
@@ -298,10 +287,7 @@ def run_native(args):
             times.append(time.perf_counter() - t)
             pairs += rep["matvecs"] * n * (n - 1) + 2 * n * nc
         tsum = sum(times)
-        if world > 1:
-            tt = torch.tensor([tsum], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tsum = float(tt.item())
+        tsum = bd.max_over_ranks(tsum, world, dev)
         line["e2e"] = {"value": pairs / tsum, "unit": UNIT, "h2d_bytes_per_step": 8 * (7 * n + 4 * nc + 2 * n),
                        "d2h_bytes_per_step": 8 * (2 * n + 1), "ms_per_step": 1e3 * tsum / ke, "steps": ke,
                        "timer": "host wall clock around synchronous C-ABI calls"}

@@ -58,8 +58,11 @@ typedef enum {
 typedef struct {
   int32_t rank, world;       /* 0 <= rank < world */
   int32_t device;            /* CUDA device ordinal this rank uses (-1: current device) */
+  int32_t flags;             /* 0, or BIPB_DIST_NO_COMM (testing: no communicator; products
+                                and b contain only this rank's rows, the rest is zero) */
   unsigned char nccl_uid[128];
 } bipb_dist;
+#define BIPB_DIST_NO_COMM 1
 
 /* GMRES report (iterations, restarts, final residual, history). */
 typedef struct {

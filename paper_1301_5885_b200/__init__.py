@@ -36,9 +36,12 @@ class BipbError(RuntimeError):
         self.status = status
 
 
+DIST_NO_COMM = 1
+
+
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("nccl_uid", ctypes.c_ubyte * 128)]
+                ("flags", ctypes.c_int32), ("nccl_uid", ctypes.c_ubyte * 128)]
 
 
 class Report(ctypes.Structure):
@@ -151,7 +154,7 @@ class Context:
 
 def bipb_setup(centroids, normals, areas, charges, eps1, eps2, kappa, dist=None, stream=None) -> Context:
     """Table 1 step 4: geometry [n,3] x2, areas [n], charges [nc,4] (x,y,z,Q).
-    dist: None or (rank, world, uid_bytes[, device]).  stream: None (library stream) or a
+    dist: None or (rank, world, uid_bytes[, device[, flags]]) (flags: DIST_NO_COMM for tests).  stream: None (library stream) or a
     cudaStream_t handle (int), e.g. torch.cuda.current_stream().cuda_stream."""
     n = int(centroids.shape[0])
     nc = int(charges.shape[0]) if charges is not None else 0
@@ -163,8 +166,10 @@ def bipb_setup(centroids, normals, areas, charges, eps1, eps2, kappa, dist=None,
     if dist is not None:
         rank, world, uid = dist[0], dist[1], dist[2]
         dev = dist[3] if len(dist) > 3 else -1
-        d = Dist(rank=rank, world=world, device=dev)
-        ctypes.memmove(d.nccl_uid, bytes(uid), 128)
+        flags = dist[4] if len(dist) > 4 else 0
+        d = Dist(rank=rank, world=world, device=dev, flags=flags)
+        if uid is not None:
+            ctypes.memmove(d.nccl_uid, bytes(uid), 128)
     h = _P()
     st = _lib.bipb_setup(ctypes.byref(h), n, pc, pn, pa, nc, pq, float(eps1), float(eps2), float(kappa),
                          ctypes.byref(d) if d is not None else None, stream)

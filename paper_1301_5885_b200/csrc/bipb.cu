@@ -96,6 +96,8 @@ struct bipb_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, world = 1;
+  bool sharded = false;  // a bipb_dist was given: stage -> all-gather -> unpack path (even at world 1)
+  bool no_comm = false;  // BIPB_DIST_NO_COMM: rows of this rank only (tests)
   ncclComm_t comm = nullptr;
 
   int64_t n = 0, nc = 0;
@@ -235,6 +237,14 @@ static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
 
 // exchange: every rank's rows [r0,r1) of the two halves -> full vector on every rank
 static bipb_status allgather_rows(bipb_ctx* c, double* y) {
+  if (c->no_comm) {  // test mode: place this rank's rows only
+    CK(cudaMemsetAsync(y, 0, 2 * c->n * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(c->gather, 0, (size_t)c->world * 2 * c->np * sizeof(double), c->stream));
+    CK(cudaMemcpyAsync(c->gather + (size_t)c->rank * 2 * c->np, c->stage, 2 * c->np * sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->stream));
+    LAUNCH1D(unpack_kernel, c->world * c->np, c->gather, c->n, c->np, c->world, y);
+    return BIPB_OK;
+  }
   NcclApi& api = nccl();
   ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)(2 * c->np), ncclFloat64, c->comm, c->stream);
   if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
@@ -259,7 +269,7 @@ static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
   a.part = c->part;
   CKS((launch_pair<MATVEC, MV_TPB, MV_T, MV_MINB>(c, a, c->nchunk_mv, 0)));
   const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
-  if (c->world == 1) {
+  if (!c->sharded) {
     LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u, u + n, d1, d2, y, y + n);
   } else {
     LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u + c->r0, u + n + c->r0, d1, d2, c->stage,
@@ -392,6 +402,8 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->s = c->screened ? kappa : 1.0;
   c->rank = dist ? dist->rank : 0;
   c->world = dist ? dist->world : 1;
+  c->sharded = dist != nullptr;
+  c->no_comm = dist && (dist->flags & BIPB_DIST_NO_COMM);
   bipb_partition(n, c->world, c->rank, &c->r0, &c->r1);
   c->np = cdiv(n, c->world);
   bipb_partition(nc, c->world, c->rank, &c->k0, &c->k1);
@@ -444,7 +456,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   CK(cudaMemsetAsync(c->red_cnt, 0, sizeof(unsigned), c->stream));
   CK(cudaMalloc(&c->dflag, sizeof(int)));
   CK(cudaMallocHost(&c->host_info, 8 * sizeof(double)));
-  if (c->world > 1) {
+  if (c->sharded) {
     const int64_t st = std::max<int64_t>(2 * c->np, c->kp);
     CK(cudaMalloc(&c->stage, st * sizeof(double)));
     CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
@@ -474,7 +486,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   }
 
   // ---- NCCL communicator
-  if (c->world > 1) {
+  if (c->sharded && !c->no_comm) {
     NcclApi& api = nccl();
     if (!api.ok) return fail(BIPB_ERR_NCCL, "libnccl.so.2 not loadable");
     ncclUniqueId id;
@@ -530,7 +542,7 @@ bipb_status bipb_source(bipb_ctx* c, double* b) {
     a.part = c->part;
     CKS((launch_pair<SOURCE, SRC_TPB, SRC_T, SRC_MINB>(c, a, c->nchunk_src, 1)));
     const double scale = 1.0 / (FOUR_PI * c->eps1);
-    if (c->world == 1) {
+    if (!c->sharded) {
       LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->b, c->b + n);
     } else {
       LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->stage, c->stage + c->np);
@@ -708,13 +720,19 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
     CKS(ensure_part(c, (size_t)(2 * c->nchunk_en * std::max<int64_t>(kloc, 1))));
     a.part = c->part;
     CKS((launch_pair<ENERGY, EN_TPB, EN_T, EN_MINB>(c, a, c->nchunk_en, 2)));
-    if (c->world == 1) {
+    if (!c->sharded) {
       LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->phit);
     } else {
       LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->stage);
-      NcclApi& api = nccl();
-      ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)c->kp, ncclFloat64, c->comm, c->stream);
-      if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+      if (c->no_comm) {
+        CK(cudaMemsetAsync(c->gather, 0, (size_t)c->world * c->kp * sizeof(double), c->stream));
+        CK(cudaMemcpyAsync(c->gather + (size_t)c->rank * c->kp, c->stage, kloc * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->stream));
+      } else {
+        NcclApi& api = nccl();
+        ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)c->kp, ncclFloat64, c->comm, c->stream);
+        if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+      }
       LAUNCH1D(unpack1_kernel, c->world * c->kp, c->gather, nc, c->kp, c->world, c->phit);
     }
     energy_sum_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(c->q4, c->phit, nc, c->red_part, c->red_cnt,

@@ -230,3 +230,63 @@ def test_device_pointers_and_determinism(bp):
     st2, rep2 = bp.bipb_gmres_solve(ctx, x2, None, 20, 1e-10, 200)
     assert torch.equal(x, x2) and rep["iterations"] == rep2["iterations"]
     ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_shards_bitwise_equal_single_gpu(bp, world):
+    """Each rank's rows (BIPB_DIST_NO_COMM: no communicator, this rank's rows only) equal the
+    single-GPU product bitwise: the chunk decomposition depends on N only."""
+    p = g.sphere_problem(3, 4.0, g.charges_in_ball(23, 3.0, 5))
+    full = _ctx(bp, p)
+    u = g.random_vector(2 * p.n, 9)
+    y1 = bp.bipb_matvec(full, u)
+    b1 = bp.bipb_source(full)
+    phi1 = np.zeros(p.nc)
+    e1 = bp.bipb_energy(full, u, phi1)
+    full.close()
+    y = np.zeros(2 * p.n)
+    b = np.zeros(2 * p.n)
+    phi = np.zeros(p.nc)
+    for r in range(world):
+        c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa,
+                          dist=(r, world, None, -1, bp.DIST_NO_COMM))
+        yr = bp.bipb_matvec(c, u)
+        br = bp.bipb_source(c)
+        ph = np.zeros(p.nc)
+        bp.bipb_energy(c, u, ph)
+        r0, r1 = bp.bipb_partition(p.n, world, r)
+        k0, k1 = bp.bipb_partition(p.nc, world, r)
+        mask = np.zeros(2 * p.n, bool)
+        mask[r0:r1] = True
+        mask[p.n + r0:p.n + r1] = True
+        assert np.all(yr[~mask] == 0) and np.all(br[~mask] == 0)
+        y[mask] = yr[mask]
+        b[mask] = br[mask]
+        phi[k0:k1] = ph[k0:k1]
+        c.close()
+    assert np.array_equal(y, y1) and np.array_equal(b, b1) and np.array_equal(phi, phi1)
+    assert e1 == pytest.approx(0.5 * 4 * np.pi * 332.0716 * float(np.dot(p.charges[:, 3], phi)), rel=1e-13)
+
+
+def test_nccl_exchange_path_world1(bp):
+    """The real NCCL exchange path (dlopen'ed libnccl, unique id, communicator, all-gather on
+    the library stream, unpack) on a world-1 communicator equals the unsharded path bitwise."""
+    import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library reuses)
+    p = g.sphere_problem(3, 4.0, g.charges_in_ball(23, 3.0, 6))
+    ref = _ctx(bp, p)
+    u = g.random_vector(2 * p.n, 2)
+    y0, b0 = bp.bipb_matvec(ref, u), bp.bipb_source(ref)
+    x0 = np.zeros(2 * p.n)
+    st0, rep0 = bp.bipb_gmres_solve(ref, x0, None, 20, 1e-10, 300)
+    e0 = bp.bipb_energy(ref, x0)
+    ref.close()
+    uid = bp.bipb_nccl_unique_id()
+    assert len(uid) == 128
+    c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=(0, 1, uid, 0))
+    assert np.array_equal(bp.bipb_matvec(c, u), y0)
+    assert np.array_equal(bp.bipb_source(c), b0)
+    x = np.zeros(2 * p.n)
+    st, rep = bp.bipb_gmres_solve(c, x, None, 20, 1e-10, 300)
+    assert rep["iterations"] == rep0["iterations"] and np.array_equal(x, x0)
+    assert bp.bipb_energy(c, x) == e0
+    c.close()
