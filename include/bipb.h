@@ -151,6 +151,21 @@ void bipb_partition(int64_t n, int32_t world, int32_t rank, int64_t* r0, int64_t
 bipb_status bipb_nccl_unique_id(unsigned char* out);
 
 /*
+ * Matvec kernel selection.  Both compute Eqs. (12)-(13) exactly (same sums,
+ * different rounding order):
+ *   0  row kernel: every ordered pair (i, j) evaluated by the thread owning row i; a row's
+ *      value is bitwise independent of the launch configuration and of the rank count.
+ *   1  symmetric kernel: each unordered pair {i, j} evaluated once and used for both rows
+ *      (K1, K4 symmetric; K2/K3 exchange under d -> -d); 28 instead of 48 FP64
+ *      instructions per ordered pair; deterministic for a fixed rank count; across ranks
+ *      the partial products are summed with ncclAllReduce.
+ * Default: 1 when the problem has at least two waves of 512 x 512 tile pairs
+ * (N >~ 11k), else 0.  BIPB_MATVEC=row|sym in the environment overrides it at setup.
+ */
+bipb_status bipb_set_matvec_kernel(bipb_ctx* ctx, int32_t kind);
+int32_t bipb_get_matvec_kernel(bipb_ctx* ctx);
+
+/*
  * Instrumentation (bench.py, tests).  `which`: 0 = matvec pair kernel, 1 = source pair
  * kernel, 2 = energy pair kernel, 3 = all kernels of the library.
  * bipb_timing_enable(ctx, 1) brackets each pair-kernel launch with CUDA events on the

@@ -67,6 +67,8 @@ _SIGS = {
     "bipb_timing_get": ([_P, _I32, ctypes.POINTER(_D), ctypes.POINTER(_I64)], ctypes.c_int),
     "bipb_timing_reset": ([_P], ctypes.c_int),
     "bipb_version": ([], ctypes.c_char_p),
+    "bipb_set_matvec_kernel": ([_P, _I32], ctypes.c_int),
+    "bipb_get_matvec_kernel": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_a, _r) in _SIGS.items():
@@ -138,6 +140,14 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    # matvec kernel selection: 0 = row kernel, 1 = symmetric-pair kernel (default) ----
+    def set_matvec_kernel(self, kind: int):
+        _check(_lib.bipb_set_matvec_kernel(self.handle, int(kind)))
+
+    @property
+    def matvec_kernel(self) -> int:
+        return int(_lib.bipb_get_matvec_kernel(self.handle))
 
     # instrumentation (bench.py) -------------------------------------------------
     def timing_enable(self, on=True):
@@ -225,6 +235,15 @@ def bipb_energy(ctx: Context, x, phi_reac=None) -> float:
     pp, _ = _ptr(phi_reac, writable=True) if phi_reac is not None else (None, None)
     _check(_lib.bipb_energy(ctx.handle, px, e.ctypes.data, pp))
     return float(e[0])
+
+
+def bipb_set_matvec_kernel(ctx: Context, kind: int):
+    """0 = row kernel (bitwise rank-count invariant), 1 = symmetric-pair kernel (bipb.h)."""
+    ctx.set_matvec_kernel(kind)
+
+
+def bipb_get_matvec_kernel(ctx: Context) -> int:
+    return ctx.matvec_kernel
 
 
 def bipb_destroy(ctx: Context):

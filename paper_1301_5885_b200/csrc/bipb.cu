@@ -14,6 +14,7 @@
 #include "../../include/bipb.h"
 #include "bipb_kernels.cuh"
 #include "bipb_vec.cuh"
+#include "bipb_sym.cuh"
 
 using namespace bipb;
 
@@ -29,6 +30,18 @@ using namespace bipb;
 #define BIPB_MV_MINB 3
 #endif
 constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
+#ifndef BIPB_SYM_TPB
+#define BIPB_SYM_TPB 128
+#endif
+#ifndef BIPB_SYM_T
+#define BIPB_SYM_T 4
+#endif
+#ifndef BIPB_SYM_MINB
+#define BIPB_SYM_MINB 1
+#endif
+constexpr int SYM_TPB = BIPB_SYM_TPB, SYM_T = BIPB_SYM_T, SYM_MINB = BIPB_SYM_MINB;
+constexpr int SYM_B = SYM_TPB * SYM_T;
+static_assert(SYM_B % TILE == 0, "symmetric block must be a multiple of the smem tile");
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
 constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
 constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
@@ -57,6 +70,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
@@ -76,9 +90,11 @@ static NcclApi& nccl() {
       api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
       api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
       api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce && api.CommDestroy &&
+               api.GetErrorString;
     }
   }
   return api;
@@ -133,6 +149,10 @@ struct bipb_ctx {
   double* host_info = nullptr;  // pinned [4]
   int* dflag = nullptr;
 
+  // symmetric matvec (bipb_sym.cuh)
+  int mv_kind = 1;  // 0 = row kernel (one evaluation per ordered pair), 1 = symmetric
+  int64_t sym_nb = 0, sym_hmax = 0, sym_W = 1, sym_runs = 1, sym_I0 = 0, sym_I1 = 0;
+  double *rec_sym = nullptr, *sym_fwd = nullptr, *sym_rev = nullptr, *sym_p = nullptr;
   int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
 
   bool timing = false;
@@ -252,8 +272,56 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
   return BIPB_OK;
 }
 
+// symmetric-pair product (bipb_sym.cuh): y = A u
+static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) {
+  const int64_t n = c->n;
+  LAUNCH1D(prescale_sym_kernel, n, u, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->rec_sym, n);
+  SymArgs a{};
+  a.rec = c->rec_sym; a.n = n; a.nb = c->sym_nb; a.B = SYM_B; a.runs = c->sym_runs; a.W = c->sym_W;
+  a.I0 = c->sym_I0; a.hmax = c->sym_hmax;
+  a.eps = c->eps; a.inveps = 1.0 / c->eps;
+  a.sc1 = c->s; a.sc2 = c->s * c->s; a.sc3 = a.sc2 * c->s;
+  a.fwd = c->sym_fwd; a.rev = c->sym_rev;
+  const int64_t nloc_blocks = c->sym_I1 - c->sym_I0;
+  if (nloc_blocks > 0) {
+    const size_t smem = sizeof(double) * (STAGES * TILE * SYM_REC + (SYM_TPB / 32) * 4 * SYM_B) + 8 * STAGES;
+    const int64_t grid = nloc_blocks * c->sym_runs;
+    if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
+    cudaEvent_t stop;
+    CKS(timed_begin(c, 0, &stop));
+    if (c->screened) {
+      auto k = sym_kernel<SYM_TPB, SYM_T, true, SYM_MINB>;
+      CKS(set_smem(k, smem));
+      k<<<(unsigned)grid, SYM_TPB, smem, c->stream>>>(a);
+    } else {
+      auto k = sym_kernel<SYM_TPB, SYM_T, false, SYM_MINB>;
+      CKS(set_smem(k, smem));
+      k<<<(unsigned)grid, SYM_TPB, smem, c->stream>>>(a);
+    }
+    CK(cudaGetLastError());
+    if (stop) CK(cudaEventRecord(stop, c->stream));
+  }
+  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
+  if (!c->sharded) {
+    LAUNCH1D(reduce_sym_kernel, n, c->sym_fwd, c->sym_rev, n, c->sym_nb, (int64_t)SYM_B, c->sym_runs, c->sym_hmax,
+             c->sym_I0, c->sym_I1, u, d1, d2, 1, y, y + n);
+    return BIPB_OK;
+  }
+  // sharded: this rank's partial sums for all rows, summed over ranks, then the row epilogue
+  LAUNCH1D(reduce_sym_kernel, n, c->sym_fwd, c->sym_rev, n, c->sym_nb, (int64_t)SYM_B, c->sym_runs, c->sym_hmax,
+           c->sym_I0, c->sym_I1, u, d1, d2, 0, c->sym_p, c->sym_p + n);
+  if (!c->no_comm) {
+    NcclApi& api = nccl();
+    ncclResult_t r = api.AllReduce(c->sym_p, c->sym_p, (size_t)(2 * n), ncclFloat64, ncclSum, c->comm, c->stream);
+    if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+  }
+  LAUNCH1D(finish_sym_kernel, n, c->sym_p, u, n, d1, d2, y);
+  return BIPB_OK;
+}
+
 // y = A u (device vectors of length 2n; y must not alias u)
 static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
+  if (c->mv_kind == 1) return matvec_sym_dev(c, u, y);
   const int64_t n = c->n;
   LAUNCH1D(prescale_kernel, n, u, c->ew, c->enx, c->eny, c->enz, c->rec_el, n);
   const int64_t nloc = c->r1 - c->r0;
@@ -338,7 +406,8 @@ void bipb_destroy(bipb_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   double* bufs[] = {c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->ew, c->rec_el, c->qx, c->qy, c->qz, c->q4,
                     c->rec_ch, c->part, c->b, c->stage, c->gather, c->ubuf, c->ybuf, c->xbuf, c->bbuf, c->tbuf,
-                    c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part};
+                    c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part,
+                    c->rec_sym, c->sym_fwd, c->sym_rev, c->sym_p};
   for (double* p : bufs)
     if (p) cudaFree(p);
   if (c->red_cnt) cudaFree(c->red_cnt);
@@ -469,6 +538,27 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->nchunk_src = cdiv(std::max<int64_t>(nc, 1), c->chunk_src);
   c->chunk_en = choose_chunk(std::max<int64_t>(nc, 1), n, EN_TPB * EN_T);
   c->nchunk_en = cdiv(n, c->chunk_en);
+
+  // ---- symmetric matvec schedule (bipb_sym.cuh): I-blocks sharded by rank
+  {
+    c->sym_nb = cdiv(n, SYM_B);
+    c->sym_hmax = (c->sym_nb & 1) ? (c->sym_nb - 1) / 2 : c->sym_nb / 2;
+    bipb_partition(c->sym_nb, c->world, c->rank, &c->sym_I0, &c->sym_I1);
+    const int64_t tiles_local = (c->sym_I1 - c->sym_I0) * (c->sym_hmax + 1);
+    c->sym_W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / WANT_CTAS));
+    c->sym_runs = cdiv(c->sym_hmax + 1, c->sym_W);
+    // default kernel: symmetric once there are >= 2 waves of (I, J) tiles, else the row kernel
+    c->mv_kind = (c->sym_nb * (c->sym_hmax + 1) >= 2 * 2 * 148) ? 1 : 0;
+    const char* env = getenv("BIPB_MATVEC");
+    if (env && (!strcmp(env, "row") || !strcmp(env, "0"))) c->mv_kind = 0;
+    if (env && (!strcmp(env, "sym") || !strcmp(env, "1"))) c->mv_kind = 1;
+    const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * SYM_REC;  // tile-SoA, padded to whole tiles
+    CK(cudaMalloc(&c->rec_sym, rec_doubles * sizeof(double)));
+    CK(cudaMemsetAsync(c->rec_sym, 0, rec_doubles * sizeof(double), c->stream));
+    CK(cudaMalloc(&c->sym_fwd, (size_t)c->sym_nb * c->sym_runs * 2 * SYM_B * sizeof(double)));
+    CK(cudaMalloc(&c->sym_rev, (size_t)c->sym_nb * (c->sym_hmax + 1) * 2 * SYM_B * sizeof(double)));
+    if (c->sharded) CK(cudaMalloc(&c->sym_p, (size_t)2 * n * sizeof(double)));
+  }
 
   // ---- singular configuration: a charge within 1e-6 A of a centroid (R11)
   if (nc > 0) {
@@ -751,6 +841,14 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
   CK(cudaStreamSynchronize(c->stream));
   return BIPB_OK;
 }
+
+bipb_status bipb_set_matvec_kernel(bipb_ctx* c, int32_t kind) {
+  if (!c || (kind != 0 && kind != 1)) return fail(BIPB_ERR_ARG, "kind must be 0 (row) or 1 (symmetric)");
+  c->mv_kind = kind;
+  return BIPB_OK;
+}
+
+int32_t bipb_get_matvec_kernel(bipb_ctx* c) { return c ? c->mv_kind : -1; }
 
 bipb_status bipb_timing_enable(bipb_ctx* c, int32_t on) {
   if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");

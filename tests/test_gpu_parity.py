@@ -52,11 +52,13 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("kappa", [g.KAPPA, 0.0])
 @pytest.mark.parametrize("name,make", CASES)
-def test_matvec_parity(bp, name, make, kappa):
+def test_matvec_parity(bp, name, make, kappa, kind):
     p = make(kappa)
     ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(kind)
     for u in (g.random_vector(2 * p.n, 11), g.random_vector(2 * p.n, 0, smooth_centroids=p.centroids)):
         y = bp.bipb_matvec(ctx, u)
         ref = oracle.matvec(p, u)
@@ -85,12 +87,14 @@ def test_source_and_energy_parity(bp, name, make):
     ctx.close()
 
 
+@pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("m", [10, 20])
 @pytest.mark.parametrize("name,make", CASES[:4])
-def test_solve_parity_small(bp, name, make, m):
+def test_solve_parity_small(bp, name, make, m, kind):
     p = make(g.KAPPA)
     ref = oracle.solve(p, restart=m, tol=1e-10)
     ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(kind)
     x = np.zeros(2 * p.n)
     bp.bipb_source(ctx)
     st, rep = bp.bipb_gmres_solve(ctx, x, None, m, 1e-10, 500, check_true=True)
@@ -238,6 +242,7 @@ def test_row_shards_bitwise_equal_single_gpu(bp, world):
     single-GPU product bitwise: the chunk decomposition depends on N only."""
     p = g.sphere_problem(3, 4.0, g.charges_in_ball(23, 3.0, 5))
     full = _ctx(bp, p)
+    full.set_matvec_kernel(0)
     u = g.random_vector(2 * p.n, 9)
     y1 = bp.bipb_matvec(full, u)
     b1 = bp.bipb_source(full)
@@ -250,6 +255,7 @@ def test_row_shards_bitwise_equal_single_gpu(bp, world):
     for r in range(world):
         c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa,
                           dist=(r, world, None, -1, bp.DIST_NO_COMM))
+        c.set_matvec_kernel(0)
         yr = bp.bipb_matvec(c, u)
         br = bp.bipb_source(c)
         ph = np.zeros(p.nc)
@@ -290,3 +296,41 @@ def test_nccl_exchange_path_world1(bp):
     assert rep["iterations"] == rep0["iterations"] and np.array_equal(x, x0)
     assert bp.bipb_energy(c, x) == e0
     c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_symmetric_shards_sum_to_single_gpu(bp, world):
+    """Symmetric kernel sharded by I-blocks (BIPB_DIST_NO_COMM): each rank returns
+    d u - P_rank / (4 pi); the rank partials sum to the single-GPU product (to rounding)."""
+    p = g.sphere_problem(4, 4.0, g.charges_in_ball(23, 3.0, 5))  # N = 5120 = 10 blocks of 512
+    full = _ctx(bp, p)
+    full.set_matvec_kernel(1)
+    u = g.random_vector(2 * p.n, 9)
+    y1 = bp.bipb_matvec(full, u)
+    full.close()
+    eps = p.eps2 / p.eps1
+    du = np.concatenate([0.5 * (1 + eps) * u[:p.n], 0.5 * (1 + 1 / eps) * u[p.n:]])
+    acc = np.zeros(2 * p.n)
+    for r in range(world):
+        c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa,
+                          dist=(r, world, None, -1, bp.DIST_NO_COMM))
+        c.set_matvec_kernel(1)
+        acc += bp.bipb_matvec(c, u) - du
+        c.close()
+    assert _rel(acc + du, y1) <= 1e-14
+
+
+@pytest.mark.parametrize("n_keep", [1, 2, 511, 512, 513, 1023, 1536, 2047, 2560, 5119])
+def test_symmetric_block_edges(bp, n_keep):
+    """Ragged block counts (odd/even nb, partial last block, nb = 1, 2) for the circulant schedule."""
+    p = _ragged(4, 4.0, n_keep, 3, np.zeros((0, 4))) if n_keep > 1 else g.Problem(
+        "n1", np.array([[1.0, 0, 0]]), np.array([[1.0, 0, 0]]), np.array([0.3]), np.zeros((0, 4)))
+    ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(1)
+    u = g.random_vector(2 * p.n, 4)
+    y = bp.bipb_matvec(ctx, u)
+    ctx.set_matvec_kernel(0)
+    y0 = bp.bipb_matvec(ctx, u)
+    ref = oracle.matvec(p, u)
+    assert _rel(y, ref) <= 1e-11 and _rel(y0, ref) <= 1e-11
+    ctx.close()

@@ -13,13 +13,13 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
-for tpb, t, minb, eb in [(128, 2, 4, 8), (128, 3, 3, 8), (128, 4, 2, 8), (64, 4, 4, 8), (64, 3, 6, 8),
-                         (128, 4, 2, 6), (256, 2, 2, 8), (64, 2, 8, 8), (128, 1, 8, 8)]:
-    VARIANTS.append({"tpb": tpb, "t": t, "minb": minb, "exp_bits": eb})
+# symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
+for tpb, t, minb in [(128, 2, 3), (128, 2, 2), (128, 3, 2), (64, 2, 6), (64, 4, 3), (128, 4, 1), (64, 2, 7), (128, 2, 4)]:
+    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8})
 
 
 def name(v):
-    return f"tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}"
+    return f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}"
 
 
 def build():
@@ -30,8 +30,12 @@ def build():
     os.makedirs(OUT, exist_ok=True)
     procs = []
     for v in VARIANTS:
-        extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
-                 f"-DBIPB_EXP_BITS={v['exp_bits']}"]
+        if v.get("kind") == "sym":
+            extra = [f"-DBIPB_SYM_TPB={v['tpb']}", f"-DBIPB_SYM_T={v['t']}", f"-DBIPB_SYM_MINB={v['minb']}",
+                     f"-DBIPB_EXP_BITS={v['exp_bits']}"]
+        else:
+            extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
+                     f"-DBIPB_EXP_BITS={v['exp_bits']}"]
         out = os.path.join(OUT, f"libbipb_{name(v)}.so")
         cmd = [b.NVCC, *b.FLAGS, *extra, "-o", out, *b.SRC, "-ldl"]
         procs.append(subprocess.Popen(cmd))
@@ -65,7 +69,7 @@ def run(cfg, reps):
     res = []
     for v in VARIANTS:
         lib = os.path.join(OUT, f"libbipb_{name(v)}.so")
-        env = dict(os.environ, BIPB_LIB=lib)
+        env = dict(os.environ, BIPB_LIB=lib, BIPB_MATVEC=v.get("kind", "row"))
         out = subprocess.run([sys.executable, __file__, "one", cfg, str(reps)], env=env, capture_output=True,
                              text=True, timeout=600)
         try:
@@ -80,7 +84,13 @@ def run(cfg, reps):
 
 if __name__ == "__main__":
     cmd = sys.argv[1]
-    if cmd == "build":
+    if cmd == "kinds":  # time the default library's two matvec kernels
+        cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
+        for kind in ("row", "sym"):
+            env = dict(os.environ, BIPB_MATVEC=kind)
+            out = subprocess.run([sys.executable, __file__, "one", cfg, "3"], env=env, capture_output=True, text=True)
+            print(kind, out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-800:], flush=True)
+    elif cmd == "build":
         build()
     elif cmd == "one":
         print(json.dumps(one(sys.argv[2], int(sys.argv[3]))))
