@@ -29,8 +29,15 @@ sys.path.insert(0, ROOT)
 
 import bipb_inputs as g  # noqa: E402
 
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 TFLOP/s at 1965 MHz
-F_REF = 111.0  # FP64 FLOPs per matvec pair of the straightforward libdevice kernel (tools/fref_probe)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # DESIGN.md §6 "Roofline": 37.2 TFLOP/s at 1965 MHz
+# Algorithmic FLOPs per ordered matvec pair-interaction: SURVEY.md §8(d) / App. C F_alg = 60 FLOP
+# (+ 1 exp + 1 rsqrt, counted here as 0 FLOP: conservative).  DESIGN.md §6.
+F_ALG = 60.0
+# FP64 FLOPs the kernels actually execute per ordered pair (ncu convention 2*DFMA + DMUL + DADD,
+# from the SASS loop bodies; profiles/r01/SUMMARY.md): row kernel 74, symmetric kernel 43.
+F_EXEC = {0: 74.0, 1: 43.0}
+KERNEL_NAME = {0: "bipb::pair_kernel<MATVEC> (row kernel)", 1: "bipb::sym_kernel (symmetric-pair kernel)"}
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r01", "traffic.json")
 METRIC = "fp64_pair_interactions_per_sec"
 UNIT = "pair-interactions/s"
 RESTART_M, TOL, MAX_IT = 20, 1e-10, 500
@@ -230,18 +237,32 @@ def run_native(args):
     matvecs = [r["matvecs"] for r in reps]
     pairs_per_step = [mv * n * (n - 1) + 2 * n * nc for mv in matvecs]
     value = sum(pairs_per_step) / (total_ms / 1e3)
-    nloc = bp.bipb_partition(n, world, rank)
-    rows_local = nloc[1] - nloc[0]
-    pairs_per_launch = rows_local * (n - 1)
+    kind = ctx.matvec_kernel
+    if kind == 1:  # symmetric: pairs evaluated by this rank = its I-blocks' share of all pairs
+        pairs_per_launch = n * (n - 1) // world
+    else:
+        r0, r1 = bp.bipb_partition(n, world, rank)
+        pairs_per_launch = (r1 - r0) * (n - 1)
     avg_launch_ms = mv_ms / max(mv_launches, 1)
-    achieved = F_REF * pairs_per_launch / (avg_launch_ms / 1e3) / 1e12
+    rate = pairs_per_launch / (avg_launch_ms / 1e3)
+    achieved = F_ALG * rate / 1e12
+    traffic = None
+    try:
+        tj = json.load(open(TRAFFIC_JSON))
+        traffic = tj.get(str(kind), {}).get("bytes_per_launch")
+    except Exception:
+        pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "bipb::pair_kernel<MATVEC> (FP64 pipe)", "flops_per_unit": F_REF,
-                "unit_of_work": "matvec pair-interaction", "units_per_launch": pairs_per_launch,
-                "avg_launch_ms": avg_launch_ms, "launches": mv_launches,
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": KERNEL_NAME[kind], "flops_per_unit": F_ALG,
+                "unit_of_work": "ordered matvec pair-interaction (i, j != i)",
+                "units_per_launch": pairs_per_launch, "avg_launch_ms": avg_launch_ms, "launches": mv_launches,
                 "kernel_share_of_step": mv_ms / max(sum(per_step_ms), 1e-9),
-                "peak_note": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (derived; DFMA microbench measured 34.2)"}
+                "executed_fp64_flops_per_unit": F_EXEC[kind],
+                "executed_fp64_frac": F_EXEC[kind] * rate / 1e12 / FP64_PEAK_TFLOPS,
+                "peak_note": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (derived); measured DMUL/DADD 99.6%, "
+                             "DFMA 90% of it (tools/fp64_peak.cu)",
+                "flops_note": "F_alg = 60 FLOP/ordered pair (SURVEY App. C), exp/rsqrt counted 0"}
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
