@@ -275,7 +275,7 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
 // symmetric-pair product (bipb_sym.cuh): y = A u
 static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) {
   const int64_t n = c->n;
-  LAUNCH1D(prescale_sym_kernel, n, u, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->rec_sym, n);
+  LAUNCH1D(prescale_sym_kernel, n, u, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->rec_sym, n, c->s);
   SymArgs a{};
   a.rec = c->rec_sym; a.n = n; a.nb = c->sym_nb; a.B = SYM_B; a.runs = c->sym_runs; a.W = c->sym_W;
   a.I0 = c->sym_I0; a.hmax = c->sym_hmax;
@@ -284,7 +284,7 @@ static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) {
   a.fwd = c->sym_fwd; a.rev = c->sym_rev;
   const int64_t nloc_blocks = c->sym_I1 - c->sym_I0;
   if (nloc_blocks > 0) {
-    const size_t smem = sizeof(double) * (STAGES * TILE * SYM_REC + (SYM_TPB / 32) * 4 * SYM_B) + 8 * STAGES;
+    const size_t smem = sizeof(double) * (STAGES * TILE * SYM_REC + (SYM_TPB / 32) * 2 * SYM_B) + 8 * STAGES;
     const int64_t grid = nloc_blocks * c->sym_runs;
     if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
     cudaEvent_t stop;

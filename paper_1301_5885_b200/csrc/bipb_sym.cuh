@@ -57,16 +57,26 @@ struct SymTgt {
   double X, Y, Z, NX, NY, NZ, C, A;
 };
 
+struct Acc2 {
+  double p0, p1;
+};
+
 // One unordered pair: target i (registers) and source j (smem record).
-// Forward into f (row i), reverse into r (row j).  d = x_i - x_j (scaled), t = |d| = kappa r,
-// a = W u_phi, c = W u_dphi.  With A = a nu every normal-weighted dot product reduces to
-// d.nu_i, d.nu_j and nu_i.nu_j:
-//   i <- j:  rho(1-e) c_j,   a_j (d.nu_j) rho^3 (eps p1 - 1),   (d.nu_i) rho^3 (1 - p1/eps) c_j,   a_j rho^3 Q
-//   j <- i:  rho(1-e) c_i,  -a_i (d.nu_i) rho^3 (eps p1 - 1),  -(d.nu_j) rho^3 (1 - p1/eps) c_i,   a_i rho^3 Q
+// Forward into f (row i), reverse into r (row j).  d = x_i - x_j (scaled by s = kappa),
+// t = |d| = kappa r, c = W u_dphi, a' = s W u_phi (the record stores a' so that the four
+// kernel sums of a row collapse into two accumulators of equal scale: p0 = K1 + K2 terms / s,
+// p1 = K3 + K4 terms / s^2).  With A = a nu every normal-weighted product reduces to d.nu_i,
+// d.nu_j and nu_i.nu_j:
+//   i <- j:  p0 += rho(1-e) c_j + a'_j (d.nu_j) rho^3 (eps p1 - 1)
+//            p1 += -(d.nu_i) rho^3 (1 - p1/eps) c_j + a'_j rho^3 Q
+//   j <- i:  p0 += rho(1-e) c_i - a'_i (d.nu_i) rho^3 (eps p1 - 1)
+//            p1 += (d.nu_j) rho^3 (1 - p1/eps) c_i + a'_i rho^3 Q
 //   Q = (p1 - 1)(nu_i.nu_j - 3 (d.nu_i)(d.nu_j) rho^2) - e (d.nu_i)(d.nu_j)   (shared by both rows)
+// kappa = 0 (s = 1): p0 = sum of the K2 geometry, p1 = sum of the K3 geometry; the constant
+// factors (eps - 1), (1 - 1/eps) are applied per row.
 template <bool SCREENED>
 __device__ __forceinline__ void pair_sym(const SymTgt& ti, const double4 s0, const double4 s1, const PairConst& k,
-                                         const double* __restrict__ tab, MvAcc& f, MvAcc& r) {
+                                         const double* __restrict__ tab, Acc2& f, Acc2& r) {
   const double dx = ti.X - s0.x, dy = ti.Y - s0.y, dz = ti.Z - s0.z;
   const double cj = s0.w, aj = s1.x;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
@@ -86,19 +96,15 @@ __device__ __forceinline__ void pair_sym(const SymTgt& ti, const double4 s0, con
     const double r3f3 = rho3 * fma(-k.inveps, p1m1, k.omie);  // rho^3 (1 - p1/eps)
     const double dd = dni * dnj;
     const double r3q = rho3 * fma(p1m1, fma(dd * rho2, -3.0, nij), -(e * dd));
-    f.a1 = fma(-rem1, cj, f.a1);
-    f.a2 = fma(aj, dnj * r3f2, f.a2);
-    f.a3 = fma(dni * r3f3, cj, f.a3);
-    f.a4 = fma(aj, r3q, f.a4);
-    r.a1 = fma(-rem1, ti.C, r.a1);
-    r.a2 = fma(-ti.A, dni * r3f2, r.a2);
-    r.a3 = fma(-(dnj * r3f3), ti.C, r.a3);
-    r.a4 = fma(ti.A, r3q, r.a4);
+    f.p0 = fma(aj, dnj * r3f2, fma(-rem1, cj, f.p0));
+    f.p1 = fma(aj, r3q, fma(-(dni * r3f3), cj, f.p1));
+    r.p0 = fma(-ti.A, dni * r3f2, fma(-rem1, ti.C, r.p0));
+    r.p1 = fma(ti.A, r3q, fma(dnj * r3f3, ti.C, r.p1));
   } else {
-    f.a2 = fma(aj, dnj * rho3, f.a2);
-    f.a3 = fma(dni * rho3, cj, f.a3);
-    r.a2 = fma(-ti.A, dni * rho3, r.a2);
-    r.a3 = fma(-(dnj * rho3), ti.C, r.a3);
+    f.p0 = fma(aj, dnj * rho3, f.p0);
+    f.p1 = fma(dni * rho3, cj, f.p1);
+    r.p0 = fma(-ti.A, dni * rho3, r.p0);
+    r.p1 = fma(-(dnj * rho3), ti.C, r.p1);
   }
 }
 
@@ -115,8 +121,8 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double s_tab[EXP_TAB];
   double* sbuf = reinterpret_cast<double*>(smem_raw);                           // [STAGES][TILE][10]
-  double* rsum = sbuf + STAGES * TILE * SYM_REC;                                  // [NW][2][B]... [NW][4][B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(rsum + NW * 4 * B);
+  double* rsum = sbuf + STAGES * TILE * SYM_REC;  // [NW][2][B] per-warp reverse sums of the current J-block
+  uint64_t* full = reinterpret_cast<uint64_t*>(rsum + NW * 2 * B);
   for (int i = threadIdx.x; i < EXP_TAB; i += TPB) s_tab[i] = c_exp_tab[i];
   const PairConst kc{a.eps, a.inveps, a.eps - 1.0, 1.0 - a.inveps};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,12 +138,12 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   // targets (registers); rows past n sit far away with c = A = 0 (exact zero reverse terms)
   SymTgt tg[T];
   int64_t gi[T];
-  MvAcc fa[T];
+  Acc2 fa[T];
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int64_t i = i0 + threadIdx.x + k * TPB;
     gi[k] = i;
-    fa[k].a1 = fa[k].a2 = fa[k].a3 = fa[k].a4 = 0.0;
+    fa[k].p0 = fa[k].p1 = 0.0;
     if (i < a.n) {
       const double* p = a.rec + sym_idx(i, 0);
       tg[k] = SymTgt{p[0], p[TILE], p[2 * TILE], p[5 * TILE], p[6 * TILE], p[7 * TILE], p[3 * TILE], p[4 * TILE]};
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
     // warp's complete reverse sum for source l: no shuffle-add reduction tree.
     for (int g0 = 0; g0 < cnt; g0 += 32) {
       const int gcnt = (cnt - g0 < 32) ? cnt - g0 : 32;
-      MvAcc rv{0.0, 0.0, 0.0, 0.0};
+      Acc2 rv{0.0, 0.0};
       if (o != 0 && gcnt == 32) {
 #pragma unroll 1
         for (int st = 0; st < 32; ++st) {
@@ -202,10 +208,8 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
           rec_load(sb, jq, s0, s1);
 #pragma unroll
           for (int k = 0; k < T; ++k) pair_sym<SCREENED>(tg[k], s0, s1, kc, s_tab, fa[k], rv);
-          rv.a1 = __shfl_sync(0xffffffffu, rv.a1, (lane + 1) & 31);
-          rv.a2 = __shfl_sync(0xffffffffu, rv.a2, (lane + 1) & 31);
-          rv.a3 = __shfl_sync(0xffffffffu, rv.a3, (lane + 1) & 31);
-          rv.a4 = __shfl_sync(0xffffffffu, rv.a4, (lane + 1) & 31);
+          rv.p0 = __shfl_sync(0xffffffffu, rv.p0, (lane + 1) & 31);
+          rv.p1 = __shfl_sync(0xffffffffu, rv.p1, (lane + 1) & 31);
         }
       } else {
         // diagonal block (pairs i < j only) or a partial group
@@ -221,18 +225,14 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
             for (int k = 0; k < T; ++k)
               if (o != 0 || gi[k] < gj) pair_sym<SCREENED>(tg[k], s0, s1, kc, s_tab, fa[k], rv);
           }
-          rv.a1 = __shfl_sync(0xffffffffu, rv.a1, (lane + 1) & 31);
-          rv.a2 = __shfl_sync(0xffffffffu, rv.a2, (lane + 1) & 31);
-          rv.a3 = __shfl_sync(0xffffffffu, rv.a3, (lane + 1) & 31);
-          rv.a4 = __shfl_sync(0xffffffffu, rv.a4, (lane + 1) & 31);
+          rv.p0 = __shfl_sync(0xffffffffu, rv.p0, (lane + 1) & 31);
+          rv.p1 = __shfl_sync(0xffffffffu, rv.p1, (lane + 1) & 31);
         }
       }
       if (lane < gcnt) {
-        double* rs = rsum + (warp * 4) * B + jl0 + g0 + lane;
-        rs[0] = rv.a1;
-        rs[B] = rv.a2;
-        rs[2 * B] = rv.a3;
-        rs[3 * B] = rv.a4;
+        double* rs = rsum + (warp * 2) * B + jl0 + g0 + lane;
+        rs[0] = rv.p0;
+        rs[B] = rv.p1;
       }
     }
     __syncthreads();  // buffer `buf` consumed; rsum entries of this stage written
@@ -244,20 +244,18 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
       double* rv1 = rv0 + B;
       for (int jl = threadIdx.x; jl < B; jl += TPB) {
         if (J * B + jl >= a.n) continue;
-        double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+        double q0 = 0.0, q1 = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-          s1 += rsum[(w * 4) * B + jl];
-          s2 += rsum[(w * 4 + 1) * B + jl];
-          s3 += rsum[(w * 4 + 2) * B + jl];
-          s4 += rsum[(w * 4 + 3) * B + jl];
+          q0 += rsum[(w * 2) * B + jl];
+          q1 += rsum[(w * 2 + 1) * B + jl];
         }
         if constexpr (SCREENED) {
-          rv0[jl] = fma(a.sc1, s1, a.sc2 * s2);
-          rv1[jl] = fma(a.sc3, s4, -(a.sc2 * s3));
+          rv0[jl] = a.sc1 * q0;
+          rv1[jl] = a.sc2 * q1;
         } else {
-          rv0[jl] = (a.eps - 1.0) * s2;
-          rv1[jl] = -((1.0 - a.inveps) * s3);
+          rv0[jl] = (a.eps - 1.0) * q0;
+          rv1[jl] = -((1.0 - a.inveps) * q1);
         }
       }
       __syncthreads();  // rsum reused by the next J-block
@@ -271,28 +269,28 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   for (int k = 0; k < T; ++k) {
     const int l = threadIdx.x + k * TPB;
     if (SCREENED) {
-      f0[l] = fma(a.sc1, fa[k].a1, a.sc2 * fa[k].a2);
-      f1[l] = fma(a.sc3, fa[k].a4, -(a.sc2 * fa[k].a3));
+      f0[l] = a.sc1 * fa[k].p0;
+      f1[l] = a.sc2 * fa[k].p1;
     } else {
-      f0[l] = (a.eps - 1.0) * fa[k].a2;
-      f1[l] = -((1.0 - a.inveps) * fa[k].a3);
+      f0[l] = (a.eps - 1.0) * fa[k].p0;
+      f1[l] = -((1.0 - a.inveps) * fa[k].p1);
     }
   }
 }
 
-// records {x s, y s, z s, c = W u_dphi, a = W u_phi, nu}
+// records {x s, y s, z s, c = W u_dphi, a' = s W u_phi, nu}
 __global__ void prescale_sym_kernel(const double* __restrict__ u, const double* __restrict__ w,
                                     const double* __restrict__ ex, const double* __restrict__ ey,
                                     const double* __restrict__ ez, const double* __restrict__ nx,
                                     const double* __restrict__ ny, const double* __restrict__ nz,
-                                    double* __restrict__ rec, int64_t n) {
+                                    double* __restrict__ rec, int64_t n, double s) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     double* r = rec + sym_idx(j, 0);
     r[0] = ex[j];
     r[TILE] = ey[j];
     r[2 * TILE] = ez[j];
     r[3 * TILE] = w[j] * u[n + j];
-    r[4 * TILE] = w[j] * u[j];
+    r[4 * TILE] = s * (w[j] * u[j]);
     r[5 * TILE] = nx[j];
     r[6 * TILE] = ny[j];
     r[7 * TILE] = nz[j];

@@ -14,7 +14,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
 # symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb in [(128, 2, 3), (128, 2, 2), (128, 3, 2), (64, 2, 6), (64, 4, 3), (128, 4, 1), (64, 2, 7), (128, 2, 4)]:
+for tpb, t, minb in [(128, 4, 1), (128, 4, 2), (128, 3, 2), (128, 3, 3), (64, 4, 4), (64, 4, 3), (128, 2, 4), (256, 2, 2)]:
     VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8})
 
 
