@@ -284,13 +284,24 @@ def run_native(args):
         hc, hn, ha, hq = pin(prob.centroids), pin(prob.normals), pin(prob.areas), pin(prob.charges)
         hx = torch.zeros(2 * n, dtype=torch.float64).pin_memory()
 
-        def e2e_step():
+        phases = {"setup": 0.0, "source": 0.0, "gmres": 0.0, "energy": 0.0, "destroy": 0.0}
+
+        def e2e_step(record=False):
+            t = [time.perf_counter()]
             c2 = bp.bipb_setup(hc, hn, ha, hq, prob.eps1, prob.eps2, prob.kappa, dist=dist_arg)
+            t.append(time.perf_counter())
             bp.bipb_source(c2)
+            t.append(time.perf_counter())
             hx.zero_()
             st, rep = bp.bipb_gmres_solve(c2, hx, None, RESTART_M, TOL, MAX_IT)
+            t.append(time.perf_counter())
             e = bp.bipb_energy(c2, hx)
+            t.append(time.perf_counter())
             c2.close()
+            t.append(time.perf_counter())
+            if record:
+                for k, a, b in zip(phases, t[:-1], t[1:]):
+                    phases[k] += (b - a) * 1e3
             return rep, e
 
         if world > 1:  # every context owns its own communicator
@@ -303,7 +314,7 @@ def run_native(args):
                 dist.barrier()
             torch.cuda.synchronize()
             t = time.perf_counter()
-            rep, e = e2e_step()
+            rep, e = e2e_step(record=True)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t)
             pairs += rep["matvecs"] * n * (n - 1) + 2 * n * nc
@@ -311,6 +322,7 @@ def run_native(args):
         tsum = bd.max_over_ranks(tsum, world, dev)
         line["e2e"] = {"value": pairs / tsum, "unit": UNIT, "h2d_bytes_per_step": 8 * (7 * n + 4 * nc + 2 * n),
                        "d2h_bytes_per_step": 8 * (2 * n + 1), "ms_per_step": 1e3 * tsum / ke, "steps": ke,
+                       "phase_ms_per_step": {k: v / ke for k, v in phases.items()},
                        "timer": "host wall clock around synchronous C-ABI calls"}
     ctx.close()
 

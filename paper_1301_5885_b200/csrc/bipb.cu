@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -161,6 +162,18 @@ struct bipb_ctx {
 };
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// BIPB_TRACE=1: host wall-clock phases of bipb_setup on stderr (tools/e2e_breakdown.py)
+struct Trace {
+  bool on = getenv("BIPB_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bipb] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
 
 // Source chunk length for a pair launch: chosen from GLOBAL sizes only, so a row's sum
 // order (and value) does not depend on the number of ranks.
@@ -423,6 +436,7 @@ void bipb_destroy(bipb_ctx* c) {
 static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, const double* normals,
                               const double* areas, int64_t nc, const double* charges, double eps1, double eps2,
                               double kappa, const bipb_dist* dist, void* cuda_stream) {
+  Trace tr;
   // ---- host-side validation (bipb.h; SURVEY.md §8(b) "Errors")
   std::vector<double> C(3 * n), Nn(3 * n), W(n), Q(4 * std::max<int64_t>(nc, 0));
   auto fetch = [&](const double* src, double* dst, size_t cnt) -> bipb_status {
@@ -465,6 +479,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     for (int j = 0; j < EXP_TAB; ++j) tab[j] = (double)exp2l(-(long double)j / EXP_TAB);
     CK(cudaMemcpyToSymbol(c_exp_tab, tab, sizeof(tab)));
   }
+  tr.mark("fetch + validate");
   c->n = n; c->nc = nc; c->eps1 = eps1; c->eps2 = eps2; c->kappa = kappa;
   c->eps = eps2 / eps1;  // reading R1
   c->screened = kappa > 0.0;
@@ -485,6 +500,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     c->own_stream = true;
   }
 
+  tr.mark("stream + exp table");
   // ---- device layout: SoA elements (scaled), records, charges
   std::vector<double> sx(n), sy(n), sz(n), nx(n), ny(n), nz(n), rec(8 * n);
   for (int64_t i = 0; i < n; ++i) {
@@ -531,6 +547,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
   }
 
+  tr.mark("upload + buffers");
   // ---- launch geometry (global sizes only => P-invariant sums)
   c->chunk_mv = choose_chunk(n, n, MV_TPB * MV_T);
   c->nchunk_mv = cdiv(n, c->chunk_mv);
@@ -560,6 +577,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     if (c->sharded) CK(cudaMalloc(&c->sym_p, (size_t)2 * n * sizeof(double)));
   }
 
+  tr.mark("symmetric-kernel buffers");
   // ---- singular configuration: a charge within 1e-6 A of a centroid (R11)
   if (nc > 0) {
     CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
@@ -575,6 +593,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     if (flag) return fail(BIPB_ERR_SINGULAR, "a charge lies within 1e-6 A of an element centroid");
   }
 
+  tr.mark("singular check");
   // ---- NCCL communicator
   if (c->sharded && !c->no_comm) {
     NcclApi& api = nccl();
@@ -585,6 +604,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
   }
   CK(cudaStreamSynchronize(c->stream));
+  tr.mark("nccl + sync");
   return BIPB_OK;
 }
 
