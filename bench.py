@@ -56,6 +56,13 @@ def parse():
     return ap.parse_args()
 
 
+def bench_config(prob, world):
+    return {"workload": prob.name, "n_elements": prob.n, "n_charges": prob.nc, "restart_m": RESTART_M, "tol": TOL,
+            "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
+            "parallelism": f"shard x{world} + one NCCL collective per matvec",
+            "l2": "flushed between steps (256 MiB)"}
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -155,7 +162,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(dts),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges)",
-            "config": {"workload": prob.name, "n_elements": prob.n, "n_charges": prob.nc},
+            "config": bench_config(prob, max(1, args.gpus)),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -268,9 +275,7 @@ def run_native(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges, bipb_inputs)",
-            "config": {"workload": prob.name, "n_elements": n, "n_charges": nc, "restart_m": RESTART_M, "tol": TOL,
-                       "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
-                       "parallelism": f"row-shard x{world} + all-gather", "l2": "flushed between steps (256 MiB)"},
+            "config": bench_config(prob, world),
             "time_to_solution_s": total_ms / args.steps / 1e3,
             "iterations": [r["iterations"] for r in reps], "matvecs": matvecs,
             "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),

@@ -21,6 +21,13 @@
 
 namespace bipb {
 
+#ifndef BIPB_SYM_PREFETCH
+#define BIPB_SYM_PREFETCH 1
+#endif
+#ifndef BIPB_SYM_UNROLL
+#define BIPB_SYM_UNROLL 1
+#endif
+constexpr int SYM_UNROLL = BIPB_SYM_UNROLL;
 constexpr int SYM_REC = 8;  // fields per source: x,y,z (scaled), c = W u_dphi, a = W u_phi, nx,ny,nz (64 B)
 // Global/shared layout is "tile-SoA": for every TILE-source tile, 8 contiguous field arrays
 // of TILE doubles.  One TMA bulk copy moves a whole tile; lanes that read different sources
@@ -201,11 +208,21 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
       const int gcnt = (cnt - g0 < 32) ? cnt - g0 : 32;
       Acc2 rv{0.0, 0.0};
       if (o != 0 && gcnt == 32) {
+#if BIPB_SYM_PREFETCH
+        // the next step's record is loaded while this step computes (software pipelining)
+        double4 n0, n1;
+        rec_load(sb, g0 + lane, n0, n1);
 #pragma unroll 1
+        for (int st = 0; st < 32; ++st) {
+          const double4 s0 = n0, s1 = n1;
+          rec_load(sb, g0 + ((lane + st + 1) & 31), n0, n1);  // wraps harmlessly at st = 31
+#else
+#pragma unroll(SYM_UNROLL)
         for (int st = 0; st < 32; ++st) {
           const int jq = g0 + ((lane + st) & 31);
           double4 s0, s1;
           rec_load(sb, jq, s0, s1);
+#endif
 #pragma unroll
           for (int k = 0; k < T; ++k) pair_sym<SCREENED>(tg[k], s0, s1, kc, s_tab, fa[k], rv);
           rv.p0 = __shfl_sync(0xffffffffu, rv.p0, (lane + 1) & 31);

@@ -14,12 +14,13 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
 # symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb in [(128, 4, 1), (128, 4, 2), (128, 3, 2), (128, 3, 3), (64, 4, 4), (64, 4, 3), (128, 2, 4), (256, 2, 2)]:
-    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8})
+for tpb, t, minb, pf, un in [(128, 4, 1, 0, 1), (128, 4, 1, 1, 1), (128, 4, 1, 0, 2), (128, 3, 2, 1, 1),
+                             (128, 2, 4, 0, 2), (128, 3, 3, 1, 1)]:
+    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un})
 
 
 def name(v):
-    return f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}"
+    return f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}_un{v.get('un', 1)}"
 
 
 def build():
@@ -32,7 +33,8 @@ def build():
     for v in VARIANTS:
         if v.get("kind") == "sym":
             extra = [f"-DBIPB_SYM_TPB={v['tpb']}", f"-DBIPB_SYM_T={v['t']}", f"-DBIPB_SYM_MINB={v['minb']}",
-                     f"-DBIPB_EXP_BITS={v['exp_bits']}"]
+                     f"-DBIPB_EXP_BITS={v['exp_bits']}", f"-DBIPB_SYM_PREFETCH={v.get('pf', 0)}",
+                     f"-DBIPB_SYM_UNROLL={v.get('un', 1)}"]
         else:
             extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}"]
