@@ -83,3 +83,84 @@ def kirkwood_energy(charges: np.ndarray, a: float, eps1: float, eps2: float, kap
         else:
             small = 0
     raise RuntimeError("Kirkwood series did not converge within nmax terms")
+
+
+def _charge_sums(points, charges, a, center, nmax):
+    """For each point x (|x - center| = r) and order n: S_n(x) = sum_k Q_k s_k^n P_n(cos g_k),
+    yielded as (n, S_n) with s_k = |y_k| / a scaled out (returns sums of Q_k (s_k/a)^n P_n)."""
+    ch = np.asarray(charges, dtype=np.float64)
+    pos = ch[:, :3] - np.asarray(center)[None, :]
+    Q = ch[:, 3]
+    s = np.linalg.norm(pos, axis=1)
+    x = np.asarray(points, dtype=np.float64) - np.asarray(center)[None, :]
+    r = np.linalg.norm(x, axis=1)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        uy = np.where(s[:, None] > 0, pos / np.where(s > 0, s, 1.0)[:, None], 0.0)
+        ux = x / np.where(r > 0, r, 1.0)[:, None]
+    cosg = np.clip(ux @ uy.T, -1.0, 1.0)  # [M, K]
+    w = np.broadcast_to(Q, cosg.shape).copy()
+    sa = s / a
+    p_prev, p_cur = None, np.ones_like(cosg)
+    for n in range(nmax + 1):
+        if n == 1:
+            p_prev, p_cur = p_cur, cosg.copy()
+        elif n > 1:
+            p_prev, p_cur = p_cur, ((2 * n - 1) * cosg * p_cur - (n - 1) * p_prev) / n
+        if n > 0:
+            w *= sa[None, :]
+        yield n, (w * p_cur).sum(axis=1), r
+
+
+def kirkwood_surface(points, charges, a, eps1, eps2, kappa, center=(0.0, 0.0, 0.0), nmax=None):
+    """Interior-limit potential phi1 and normal derivative d(phi1)/dr at points with
+    |x - center| <= a (the quantities the BEM unknowns approximate; Eq. (15) uses
+    phi^exa "by Kirkwood's spherical harmonic expansion").  Internal units of
+    reading R3 (q/(4 pi eps1 r) Coulomb).  SURVEY.md App. A.3:
+      phi1(x) = sum_k Q_k / (4 pi eps1 |x - y_k|)
+              + sum_n r^n f_n / (4 pi eps1 a^(2n+1)) sum_k Q_k s_k^n P_n(cos g_k).
+    Returns (phi1, dphi1_dr) arrays."""
+    ch = np.asarray(charges, dtype=np.float64)
+    x = np.asarray(points, dtype=np.float64)
+    if nmax is None:
+        smax = np.max(np.linalg.norm(ch[:, :3] - np.asarray(center)[None, :], axis=1)) / a
+        nmax = int(min(400, max(10, np.ceil(np.log(1e-17) / np.log(max(smax, 1e-3))) + 5)))
+    f = f_coeff(nmax, eps1, eps2, kappa, a)
+    d = x[:, None, :] - ch[None, :, :3]
+    dist = np.linalg.norm(d, axis=2)
+    xc = x - np.asarray(center)[None, :]
+    r = np.linalg.norm(xc, axis=1)
+    rhat = xc / np.where(r > 0, r, 1.0)[:, None]
+    phi = (ch[None, :, 3] / (4 * np.pi * eps1 * dist)).sum(axis=1)
+    dphi = (-ch[None, :, 3] * np.einsum("mkc,mc->mk", d, rhat) / (4 * np.pi * eps1 * dist ** 3)).sum(axis=1)
+    for n, S, rr in _charge_sums(x, ch, a, center, nmax):
+        # S = sum_k Q_k (s_k/a)^n P_n ; reaction term r^n f_n/(4 pi eps1 a^(2n+1)) sum Q s^n P_n
+        #   = f_n/(4 pi eps1 a) (r/a)^n S
+        ra = rr / a
+        phi = phi + f[n] / (4 * np.pi * eps1 * a) * ra ** n * S
+        if n > 0:
+            dphi = dphi + f[n] / (4 * np.pi * eps1 * a) * n * ra ** (n - 1) / a * S
+    return phi, dphi
+
+
+def kirkwood_exterior(points, charges, a, eps1, eps2, kappa, center=(0.0, 0.0, 0.0), nmax=60):
+    """Exterior potential phi2 and d(phi2)/dr at |x - center| = r >= a (same expansion, matched
+    at r = a: C_n k_n(kappa a) = A_n (1 + f_n)); used to pin the interface conditions Eq. (3)."""
+    ch = np.asarray(charges, dtype=np.float64)
+    f = f_coeff(nmax, eps1, eps2, kappa, a)
+    g = g_ratio(nmax, kappa * a)
+    phi = 0.0
+    dphi = 0.0
+    for n, S, rr in _charge_sums(points, ch, a, center, nmax):
+        An = S / (4 * np.pi * eps1 * a)  # sum_k Q_k s_k^n P_n / (4 pi eps1 a^(n+1)) in units of a^n
+        if kappa == 0.0:
+            rad, drad = (a / rr) ** (n + 1), -(n + 1) / rr * (a / rr) ** (n + 1)
+        else:
+            from scipy.special import kv
+            kn = lambda z: kv(n + 0.5, z) / np.sqrt(z)
+            rad = kn(kappa * rr) / kn(kappa * a)
+            # d/dr k_n(kappa r) / k_n(kappa a) at r: central difference of the library Bessel
+            h = 1e-6 * rr
+            drad = (kn(kappa * (rr + h)) - kn(kappa * (rr - h))) / (2 * h) / kn(kappa * a)
+        phi = phi + An * (1 + f[n]) * rad
+        dphi = dphi + An * (1 + f[n]) * drad
+    return phi, dphi, g
