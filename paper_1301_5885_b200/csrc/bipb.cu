@@ -572,8 +572,9 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * SYM_REC;  // tile-SoA, padded to whole tiles
     CK(cudaMalloc(&c->rec_sym, rec_doubles * sizeof(double)));
     CK(cudaMemsetAsync(c->rec_sym, 0, rec_doubles * sizeof(double), c->stream));
-    CK(cudaMalloc(&c->sym_fwd, (size_t)c->sym_nb * c->sym_runs * 2 * SYM_B * sizeof(double)));
-    CK(cudaMalloc(&c->sym_rev, (size_t)c->sym_nb * (c->sym_hmax + 1) * 2 * SYM_B * sizeof(double)));
+    const int64_t nbl = std::max<int64_t>(1, c->sym_I1 - c->sym_I0);  // partials only for this rank's I-blocks
+    CK(cudaMalloc(&c->sym_fwd, (size_t)nbl * c->sym_runs * 2 * SYM_B * sizeof(double)));
+    CK(cudaMalloc(&c->sym_rev, (size_t)nbl * (c->sym_hmax + 1) * 2 * SYM_B * sizeof(double)));
     if (c->sharded) CK(cudaMalloc(&c->sym_p, (size_t)2 * n * sizeof(double)));
   }
 

@@ -45,8 +45,8 @@ struct SymArgs {
   int64_t hmax;       // max offsets per I (for Rev indexing)
   double eps, inveps;
   double sc1, sc2, sc3;
-  double* fwd;        // [nb][runs][2][B]
-  double* rev;        // [nb][hmax+1][2][B]
+  double* fwd;        // [I1-I0][runs][2][B]    forward sums of tile run (I, run), rank-local I
+  double* rev;        // [I1-I0][hmax+1][2][B]  reverse sums of tile (I, J = I+o), rank-local I
 };
 
 // number of offsets (including the diagonal o = 0) for block I in the circulant schedule
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
     if ((q + 1) % stages_per_block == 0) {
       // end of J-block: combine warps (fixed order), fold s powers, write Rev[J][o]
       const int64_t J = (I + o) % a.nb;
-      double* rv0 = a.rev + ((J * (a.hmax + 1) + o) * 2) * B;
+      double* rv0 = a.rev + (((I - a.I0) * (a.hmax + 1) + o) * 2) * B;  // stored at the tile's I (rank-local)
       double* rv1 = rv0 + B;
       for (int jl = threadIdx.x; jl < B; jl += TPB) {
         if (J * B + jl >= a.n) continue;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   }
 
   // forward partials of this run
-  double* f0 = a.fwd + ((I * a.runs + run) * 2) * B;
+  double* f0 = a.fwd + (((I - a.I0) * a.runs + run) * 2) * B;
   double* f1 = f0 + B;
 #pragma unroll
   for (int k = 0; k < T; ++k) {
@@ -327,7 +327,7 @@ __global__ void reduce_sym_kernel(const double* __restrict__ fwd, const double* 
     double s0 = 0.0, s1 = 0.0;
     if (b >= I0 && b < I1) {
       for (int64_t r = 0; r < runs; ++r) {
-        const double* f = fwd + ((b * runs + r) * 2) * B;
+        const double* f = fwd + (((b - I0) * runs + r) * 2) * B;
         s0 += f[l];
         s1 += f[B + l];
       }
@@ -335,7 +335,7 @@ __global__ void reduce_sym_kernel(const double* __restrict__ fwd, const double* 
     for (int64_t o = 0; o <= hmax; ++o) {
       const int64_t I = ((b - o) % nb + nb) % nb;
       if (o >= sym_noff(I, nb) || I < I0 || I >= I1) continue;
-      const double* rv = rev + ((b * (hmax + 1) + o) * 2) * B;
+      const double* rv = rev + (((I - I0) * (hmax + 1) + o) * 2) * B;
       s0 += rv[l];
       s1 += rv[B + l];
     }
