@@ -97,6 +97,14 @@ bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const
                        double kappa, const bipb_dist* dist, void* cuda_stream);
 
 /*
+ * bipb_set_charges — replace the point charges (x, y, z, Q) [nc][4] of a context while keeping
+ * its surface, buffers and communicator (multi-RHS workflows: several charge sets or states on
+ * one surface).  The stored right-hand side is invalidated (call
+ * bipb_source again).  Errors as bipb_setup (ERR_ARG, ERR_INPUT, ERR_SINGULAR).
+ */
+bipb_status bipb_set_charges(bipb_ctx* ctx, int64_t nc, const double* charges);
+
+/*
  * bipb_source — Eq. (11), Table 1 step 6: b_i = S1(x_i), b_{i+N} = S2(x_i)
  * over all N_c charges (N x N_c pairs).  The result is kept inside the context (it is
  * the default right-hand side of bipb_gmres_solve) and, if b != NULL, written to b [2n].
@@ -110,6 +118,15 @@ bipb_status bipb_source(bipb_ctx* ctx, double* b);
  * u, y: [2n] (must not alias).  N(N-1) pair evaluations, matrix-free.
  */
 bipb_status bipb_matvec(bipb_ctx* ctx, const double* u, double* y);
+
+/*
+ * bipb_matvec_batch — the product of Eqs. (12)-(13) for nrhs operands at once (multi-RHS,
+ * several charge sets / states on one surface):
+ *   Y[r] = A U[r],  U, Y: [nrhs][2n] contiguous (must not alias).
+ * With the symmetric kernel the distance, 1/r, exp and kernel factors of a pair are evaluated
+ * once for up to 4 operands (passes of 4, 2, 1); with the row kernel it loops.
+ */
+bipb_status bipb_matvec_batch(bipb_ctx* ctx, int32_t nrhs, const double* U, double* Y);
 
 /*
  * bipb_gmres_solve — restarted GMRES(m) with modified Gram-Schmidt Arnoldi and Givens
@@ -127,6 +144,18 @@ bipb_status bipb_matvec(bipb_ctx* ctx, const double* u, double* y);
  */
 bipb_status bipb_gmres_solve(bipb_ctx* ctx, const double* b, double* x, int32_t restart_m, double tol,
                              int32_t max_iters, int32_t check_true, bipb_report* rep);
+
+/*
+ * bipb_gmres_solve_batch — nrhs independent systems A X[r] = B[r] (multi-RHS, §8(f) item 2):
+ * each runs exactly the GMRES(m) of bipb_gmres_solve (same iterates up to the rounding of the
+ * shared products); the systems advance in lockstep so every Arnoldi step applies A to all of
+ * them through one bipb_matvec_batch-style product.
+ *   B, X: [nrhs][2n] (host or device); X holds the initial guesses and receives the solutions.
+ *   reps: NULL or an array of nrhs reports.
+ * Returns BIPB_NOT_CONVERGED if any system hit max_iters (all X and reports still filled).
+ */
+bipb_status bipb_gmres_solve_batch(bipb_ctx* ctx, int32_t nrhs, const double* B, double* X, int32_t restart_m,
+                                   double tol, int32_t max_iters, int32_t check_true, bipb_report* reps);
 
 /*
  * bipb_energy — Eq. (14), Table 1 steps 18-21:

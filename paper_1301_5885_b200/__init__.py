@@ -68,6 +68,9 @@ _SIGS = {
     "bipb_timing_reset": ([_P], ctypes.c_int),
     "bipb_version": ([], ctypes.c_char_p),
     "bipb_set_matvec_kernel": ([_P, _I32], ctypes.c_int),
+    "bipb_matvec_batch": ([_P, _I32, _P, _P], ctypes.c_int),
+    "bipb_gmres_solve_batch": ([_P, _I32, _P, _P, _I32, _D, _I32, _I32, ctypes.POINTER(Report)], ctypes.c_int),
+    "bipb_set_charges": ([_P, _I64, _P], ctypes.c_int),
     "bipb_get_matvec_kernel": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
@@ -208,6 +211,51 @@ def bipb_matvec(ctx: Context, u, y=None):
     py, _ = _ptr(y, writable=True)
     _check(_lib.bipb_matvec(ctx.handle, pu, py))
     return y
+
+
+def bipb_matvec_batch(ctx: Context, U, Y=None):
+    """Multi-RHS product: Y[r] = A U[r], U and Y of shape [nrhs, 2n] (C-contiguous)."""
+    nrhs = int(U.shape[0])
+    if Y is None:
+        Y = np.empty((nrhs, 2 * ctx.n))
+    pu, _ = _ptr(U)
+    py, _ = _ptr(Y, writable=True)
+    _check(_lib.bipb_matvec_batch(ctx.handle, nrhs, pu, py))
+    return Y
+
+
+def bipb_set_charges(ctx: Context, charges):
+    """Replace the point charges [nc, 4] (x, y, z, Q) on the same surface."""
+    nc = int(charges.shape[0])
+    pq, _ = _ptr(charges) if nc > 0 else (None, None)
+    _check(_lib.bipb_set_charges(ctx.handle, nc, pq))
+    ctx.nc = nc
+
+
+def bipb_gmres_solve_batch(ctx: Context, B, X, restart_m=20, tol=1e-10, max_iters=500, check_true=False,
+                           history_cap=None):
+    """Multi-RHS GMRES: solves A X[r] = B[r] for all r in lockstep (X: initial guesses in, solutions
+    out).  Returns (status, [report dict per system])."""
+    nrhs = int(B.shape[0])
+    cap = max_iters + 1 if history_cap is None else history_cap
+    hist = np.zeros((nrhs, max(cap, 1)))
+    reps = (Report * nrhs)()
+    for r in range(nrhs):
+        reps[r].history = hist[r].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        reps[r].history_cap = cap
+    pb, _ = _ptr(B)
+    px, _ = _ptr(X, writable=True)
+    st = _lib.bipb_gmres_solve_batch(ctx.handle, nrhs, pb, px, int(restart_m), float(tol), int(max_iters),
+                                     int(check_true), reps)
+    if st not in (OK, NOT_CONVERGED):
+        _check(st)
+    out = []
+    for r in range(nrhs):
+        rp = reps[r]
+        out.append({"iterations": rp.iterations, "restarts": rp.restarts, "matvecs": rp.matvecs,
+                    "converged": bool(rp.converged), "rel_res_est": rp.rel_res_est, "rel_res_true": rp.rel_res_true,
+                    "history": hist[r, :min(rp.history_len, cap)].copy()})
+    return st, out
 
 
 def bipb_gmres_solve(ctx: Context, x, b=None, restart_m=20, tol=1e-10, max_iters=500, check_true=False,

@@ -31,6 +31,7 @@ using namespace bipb;
 #define BIPB_MV_MINB 3
 #endif
 constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
+// symmetric kernel launch shapes per number of right-hand sides R (B = TPB*T rows per block)
 #ifndef BIPB_SYM_TPB
 #define BIPB_SYM_TPB 128
 #endif
@@ -40,9 +41,21 @@ constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
 #ifndef BIPB_SYM_MINB
 #define BIPB_SYM_MINB 1
 #endif
-constexpr int SYM_TPB = BIPB_SYM_TPB, SYM_T = BIPB_SYM_T, SYM_MINB = BIPB_SYM_MINB;
-constexpr int SYM_B = SYM_TPB * SYM_T;
-static_assert(SYM_B % TILE == 0, "symmetric block must be a multiple of the smem tile");
+template <int R>
+struct SymCfg;
+template <>
+struct SymCfg<1> {
+  static constexpr int TPB = BIPB_SYM_TPB, T = BIPB_SYM_T, MINB = BIPB_SYM_MINB;
+};
+template <>
+struct SymCfg<2> {
+  static constexpr int TPB = 128, T = 2, MINB = 1;
+};
+template <>
+struct SymCfg<4> {
+  static constexpr int TPB = 128, T = 2, MINB = 1;
+};
+static_assert((SymCfg<1>::TPB * SymCfg<1>::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
 constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
 constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
@@ -136,6 +149,7 @@ struct bipb_ctx {
   double* b = nullptr;
   bool have_b = false;
   double* stage = nullptr;   // [2 np] or [kp]
+  int64_t stage_cap = 0;
   double* gather = nullptr;  // [world][2 np]
   double *ubuf = nullptr, *ybuf = nullptr, *xbuf = nullptr, *bbuf = nullptr, *tbuf = nullptr;
   double* phit = nullptr;  // [nc]
@@ -150,15 +164,22 @@ struct bipb_ctx {
   double* host_info = nullptr;  // pinned [4]
   int* dflag = nullptr;
 
-  // symmetric matvec (bipb_sym.cuh)
+  // symmetric matvec (bipb_sym.cuh): one schedule per R in {1, 2, 4}
   int mv_kind = 1;  // 0 = row kernel (one evaluation per ordered pair), 1 = symmetric
-  int64_t sym_nb = 0, sym_hmax = 0, sym_W = 1, sym_runs = 1, sym_I0 = 0, sym_I1 = 0;
-  double *rec_sym = nullptr, *sym_fwd = nullptr, *sym_rev = nullptr, *sym_p = nullptr;
+  struct SymPlan {
+    int R = 0;
+    int64_t B = 0, nb = 0, hmax = 0, W = 1, runs = 1, I0 = 0, I1 = 0, group = 1;
+    double *rec = nullptr, *fwd = nullptr, *rev = nullptr;
+  } sym[3];
+  double* sym_P = nullptr;  // [4][2][n] running row sums
+  double* bat_U = nullptr;  // [4][2n] batch staging (host inputs)
+  double* bat_Y = nullptr;
   int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
 
   bool timing = false;
   EventPool pool[3];
   int64_t launches_all = 0;
+  int64_t matvec_calls = 0;  // operator applications (for per-product kernel time)
 };
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -285,52 +306,90 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
   return BIPB_OK;
 }
 
-// symmetric-pair product (bipb_sym.cuh): y = A u
-static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) {
+// ---- symmetric-pair products (bipb_sym.cuh) ------------------------------------------------
+static int sym_slot(int R) { return R == 1 ? 0 : (R == 2 ? 1 : 2); }
+
+// Per-R schedule (global sizes; this rank's I-blocks) and buffers, allocated on first use.
+// Partials are bounded by BIPB_SYM_MEM_GB (default 4) by launching the rank's I-blocks in groups.
+template <int R>
+static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
+  bipb_ctx::SymPlan& p = c->sym[sym_slot(R)];
+  *out = &p;
+  if (p.R == R) return BIPB_OK;
+  constexpr int B = SymCfg<R>::TPB * SymCfg<R>::T;
+  constexpr int F = SymLayout<R>::F;
   const int64_t n = c->n;
-  LAUNCH1D(prescale_sym_kernel, n, u, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->rec_sym, n, c->s);
+  p.B = B;
+  p.nb = cdiv(n, B);
+  p.hmax = (p.nb & 1) ? (p.nb - 1) / 2 : p.nb / 2;
+  bipb_partition(p.nb, c->world, c->rank, &p.I0, &p.I1);
+  const int64_t tiles_local = (p.I1 - p.I0) * (p.hmax + 1);
+  p.W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / WANT_CTAS));
+  p.runs = cdiv(p.hmax + 1, p.W);
+  double gb = 4.0;
+  if (const char* e = getenv("BIPB_SYM_MEM_GB")) gb = std::max(0.001, atof(e));
+  const double per_block = (double)((p.hmax + 1) + p.runs) * R * 2 * B * sizeof(double);
+  p.group = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(p.I1 - p.I0, 1), (int64_t)(gb * 1e9 / per_block)));
+  const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * F;  // tile-SoA, padded to whole tiles
+  CK(cudaMalloc(&p.rec, rec_doubles * sizeof(double)));
+  CK(cudaMemsetAsync(p.rec, 0, rec_doubles * sizeof(double), c->stream));
+  CK(cudaMalloc(&p.fwd, (size_t)p.group * p.runs * R * 2 * B * sizeof(double)));
+  CK(cudaMalloc(&p.rev, (size_t)p.group * (p.hmax + 1) * R * 2 * B * sizeof(double)));
+  if (!c->sym_P) CK(cudaMalloc(&c->sym_P, (size_t)4 * 2 * n * sizeof(double)));
+  p.R = R;
+  return BIPB_OK;
+}
+
+// Y[r] = A U[r] for r < R (device, [R][2n] each; Y must not alias U)
+template <int R>
+static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
+  using Cfg = SymCfg<R>;
+  const int64_t n = c->n;
+  bipb_ctx::SymPlan* p;
+  CKS(sym_plan<R>(c, &p));
+  LAUNCH1D(prescale_sym_kernel<R>, n, U, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, p->rec, n, c->s);
   SymArgs a{};
-  a.rec = c->rec_sym; a.n = n; a.nb = c->sym_nb; a.B = SYM_B; a.runs = c->sym_runs; a.W = c->sym_W;
-  a.I0 = c->sym_I0; a.hmax = c->sym_hmax;
+  a.rec = p->rec; a.n = n; a.nb = p->nb; a.B = p->B; a.runs = p->runs; a.W = p->W; a.hmax = p->hmax;
   a.eps = c->eps; a.inveps = 1.0 / c->eps;
-  a.sc1 = c->s; a.sc2 = c->s * c->s; a.sc3 = a.sc2 * c->s;
-  a.fwd = c->sym_fwd; a.rev = c->sym_rev;
-  const int64_t nloc_blocks = c->sym_I1 - c->sym_I0;
-  if (nloc_blocks > 0) {
-    const size_t smem = sizeof(double) * (STAGES * TILE * SYM_REC + (SYM_TPB / 32) * 2 * SYM_B) + 8 * STAGES;
-    const int64_t grid = nloc_blocks * c->sym_runs;
+  a.sc1 = c->s; a.sc2 = c->s * c->s;
+  a.fwd = p->fwd; a.rev = p->rev;
+  const size_t smem =
+      sizeof(double) * (STAGES * TILE * SymLayout<R>::F + (Cfg::TPB / 32) * R * 2 * p->B) + 8 * STAGES;
+  if (p->I1 <= p->I0) CK(cudaMemsetAsync(c->sym_P, 0, (size_t)R * 2 * n * sizeof(double), c->stream));
+  for (int64_t Ia = p->I0; Ia < p->I1; Ia += p->group) {
+    const int64_t Ib = std::min(Ia + p->group, p->I1);
+    a.I0 = Ia;
+    const int64_t grid = (Ib - Ia) * p->runs;
     if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
     cudaEvent_t stop;
     CKS(timed_begin(c, 0, &stop));
     if (c->screened) {
-      auto k = sym_kernel<SYM_TPB, SYM_T, true, SYM_MINB>;
+      auto k = sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R>;
       CKS(set_smem(k, smem));
-      k<<<(unsigned)grid, SYM_TPB, smem, c->stream>>>(a);
+      k<<<(unsigned)grid, Cfg::TPB, smem, c->stream>>>(a);
     } else {
-      auto k = sym_kernel<SYM_TPB, SYM_T, false, SYM_MINB>;
+      auto k = sym_kernel<Cfg::TPB, Cfg::T, false, Cfg::MINB, R>;
       CKS(set_smem(k, smem));
-      k<<<(unsigned)grid, SYM_TPB, smem, c->stream>>>(a);
+      k<<<(unsigned)grid, Cfg::TPB, smem, c->stream>>>(a);
     }
     CK(cudaGetLastError());
     if (stop) CK(cudaEventRecord(stop, c->stream));
+    LAUNCH1D(reduce_sym_kernel<R>, n, p->fwd, p->rev, n, p->nb, p->B, p->runs, p->hmax, Ia, Ib, Ia == p->I0 ? 1 : 0,
+             c->sym_P);
   }
-  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
-  if (!c->sharded) {
-    LAUNCH1D(reduce_sym_kernel, n, c->sym_fwd, c->sym_rev, n, c->sym_nb, (int64_t)SYM_B, c->sym_runs, c->sym_hmax,
-             c->sym_I0, c->sym_I1, u, d1, d2, 1, y, y + n);
-    return BIPB_OK;
-  }
-  // sharded: this rank's partial sums for all rows, summed over ranks, then the row epilogue
-  LAUNCH1D(reduce_sym_kernel, n, c->sym_fwd, c->sym_rev, n, c->sym_nb, (int64_t)SYM_B, c->sym_runs, c->sym_hmax,
-           c->sym_I0, c->sym_I1, u, d1, d2, 0, c->sym_p, c->sym_p + n);
-  if (!c->no_comm) {
+  if (c->sharded && !c->no_comm) {  // every rank holds partial sums for all rows
     NcclApi& api = nccl();
-    ncclResult_t r = api.AllReduce(c->sym_p, c->sym_p, (size_t)(2 * n), ncclFloat64, ncclSum, c->comm, c->stream);
+    ncclResult_t r =
+        api.AllReduce(c->sym_P, c->sym_P, (size_t)(R * 2 * n), ncclFloat64, ncclSum, c->comm, c->stream);
     if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
   }
-  LAUNCH1D(finish_sym_kernel, n, c->sym_p, u, n, d1, d2, y);
+  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
+  LAUNCH1D(finish_sym_kernel<R>, n, c->sym_P, U, n, d1, d2, Y);
+  c->matvec_calls += R;
   return BIPB_OK;
 }
+
+static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) { return matvec_sym_R<1>(c, u, y); }
 
 // y = A u (device vectors of length 2n; y must not alias u)
 static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
@@ -349,6 +408,7 @@ static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
   CKS(ensure_part(c, (size_t)(2 * c->nchunk_mv * std::max<int64_t>(nloc, 1))));
   a.part = c->part;
   CKS((launch_pair<MATVEC, MV_TPB, MV_T, MV_MINB>(c, a, c->nchunk_mv, 0)));
+  c->matvec_calls += 1;
   const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
   if (!c->sharded) {
     LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u, u + n, d1, d2, y, y + n);
@@ -420,9 +480,14 @@ void bipb_destroy(bipb_ctx* c) {
   double* bufs[] = {c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->ew, c->rec_el, c->qx, c->qy, c->qz, c->q4,
                     c->rec_ch, c->part, c->b, c->stage, c->gather, c->ubuf, c->ybuf, c->xbuf, c->bbuf, c->tbuf,
                     c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part,
-                    c->rec_sym, c->sym_fwd, c->sym_rev, c->sym_p};
+                    c->sym_P, c->bat_U, c->bat_Y};
   for (double* p : bufs)
     if (p) cudaFree(p);
+  for (auto& sp : c->sym) {
+    if (sp.rec) cudaFree(sp.rec);
+    if (sp.fwd) cudaFree(sp.fwd);
+    if (sp.rev) cudaFree(sp.rev);
+  }
   if (c->red_cnt) cudaFree(c->red_cnt);
   if (c->dflag) cudaFree(c->dflag);
   if (c->host_info) cudaFreeHost(c->host_info);
@@ -431,6 +496,59 @@ void bipb_destroy(bipb_ctx* c) {
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+// (Re)load the point charges [nc][4] (host, validated): scaled SoA targets + records, raw copy,
+// rank partition, exchange buffers, source/energy chunking, singular check (reading R11).
+static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<double>& Q) {
+  double* olds[] = {c->qx, c->qy, c->qz, c->rec_ch, c->q4, c->phit, c->phi};
+  for (double* p : olds)
+    if (p) cudaFree(p);
+  c->qx = c->qy = c->qz = c->rec_ch = c->q4 = c->phit = c->phi = nullptr;
+  const int64_t ncm = std::max<int64_t>(nc, 1);
+  std::vector<double> qxs(ncm, 0.0), qys(ncm, 0.0), qzs(ncm, 0.0), qrec(4 * ncm, 0.0), q4(4 * ncm, 0.0);
+  for (int64_t k = 0; k < nc; ++k) {
+    qxs[k] = Q[4 * k] * c->s; qys[k] = Q[4 * k + 1] * c->s; qzs[k] = Q[4 * k + 2] * c->s;
+    qrec[4 * k] = qxs[k]; qrec[4 * k + 1] = qys[k]; qrec[4 * k + 2] = qzs[k]; qrec[4 * k + 3] = Q[4 * k + 3];
+    for (int d = 0; d < 4; ++d) q4[4 * k + d] = Q[4 * k + d];
+  }
+  auto up = [&](double** d, const std::vector<double>& h) -> bipb_status {
+    CK(cudaMalloc(d, h.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return BIPB_OK;
+  };
+  CKS(up(&c->qx, qxs)); CKS(up(&c->qy, qys)); CKS(up(&c->qz, qzs));
+  CKS(up(&c->rec_ch, qrec)); CKS(up(&c->q4, q4));
+  CK(cudaMalloc(&c->phit, ncm * sizeof(double)));
+  CK(cudaMalloc(&c->phi, ncm * sizeof(double)));
+  c->nc = nc;
+  c->have_b = false;
+  bipb_partition(nc, c->world, c->rank, &c->k0, &c->k1);
+  c->kp = cdiv(ncm, c->world);
+  if (c->sharded) {
+    const int64_t st = std::max<int64_t>(2 * c->np, c->kp);
+    if (st > c->stage_cap) {
+      if (c->stage) cudaFree(c->stage);
+      if (c->gather) cudaFree(c->gather);
+      c->stage = c->gather = nullptr;
+      CK(cudaMalloc(&c->stage, st * sizeof(double)));
+      CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
+      c->stage_cap = st;
+    }
+  }
+  c->chunk_src = choose_chunk(c->n, ncm, SRC_TPB * SRC_T);
+  c->nchunk_src = cdiv(ncm, c->chunk_src);
+  c->chunk_en = choose_chunk(ncm, c->n, EN_TPB * EN_T);
+  c->nchunk_en = cdiv(c->n, c->chunk_en);
+  if (nc > 0) {  // a charge within 1e-6 A of a centroid (compared in scaled coordinates)
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
+    LAUNCH1D(min_dist_kernel, c->n, c->ex, c->ey, c->ez, c->n, c->rec_ch, nc, 1e-12 * c->s * c->s, c->dflag);
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (flag) return fail(BIPB_ERR_SINGULAR, "a charge lies within 1e-6 A of an element centroid");
+  }
+  return BIPB_OK;
 }
 
 static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, const double* normals,
@@ -490,8 +608,6 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->no_comm = dist && (dist->flags & BIPB_DIST_NO_COMM);
   bipb_partition(n, c->world, c->rank, &c->r0, &c->r1);
   c->np = cdiv(n, c->world);
-  bipb_partition(nc, c->world, c->rank, &c->k0, &c->k1);
-  c->kp = cdiv(std::max<int64_t>(nc, 1), c->world);
 
   if (cuda_stream) {
     c->stream = (cudaStream_t)cuda_stream;
@@ -509,13 +625,6 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     rec[8 * i] = sx[i]; rec[8 * i + 1] = sy[i]; rec[8 * i + 2] = sz[i];
     for (int d = 3; d < 8; ++d) rec[8 * i + d] = 0.0;
   }
-  const int64_t ncm = std::max<int64_t>(nc, 1);
-  std::vector<double> qxs(ncm, 0.0), qys(ncm, 0.0), qzs(ncm, 0.0), qrec(4 * ncm, 0.0), q4(4 * ncm, 0.0);
-  for (int64_t k = 0; k < nc; ++k) {
-    qxs[k] = Q[4 * k] * c->s; qys[k] = Q[4 * k + 1] * c->s; qzs[k] = Q[4 * k + 2] * c->s;
-    qrec[4 * k] = qxs[k]; qrec[4 * k + 1] = qys[k]; qrec[4 * k + 2] = qzs[k]; qrec[4 * k + 3] = Q[4 * k + 3];
-    for (int d = 0; d < 4; ++d) q4[4 * k + d] = Q[4 * k + d];
-  }
   auto up = [&](double** d, const std::vector<double>& h) -> bipb_status {
     CK(cudaMalloc(d, h.size() * sizeof(double)));
     CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -524,8 +633,6 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   CKS(up(&c->ex, sx)); CKS(up(&c->ey, sy)); CKS(up(&c->ez, sz));
   CKS(up(&c->enx, nx)); CKS(up(&c->eny, ny)); CKS(up(&c->enz, nz));
   CKS(up(&c->ew, W)); CKS(up(&c->rec_el, rec));
-  CKS(up(&c->qx, qxs)); CKS(up(&c->qy, qys)); CKS(up(&c->qz, qzs));
-  CKS(up(&c->rec_ch, qrec)); CKS(up(&c->q4, q4));
   const int64_t m2 = 2 * n;
   CK(cudaMalloc(&c->b, m2 * sizeof(double)));
   CK(cudaMalloc(&c->ubuf, m2 * sizeof(double)));
@@ -533,67 +640,36 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   CK(cudaMalloc(&c->xbuf, m2 * sizeof(double)));
   CK(cudaMalloc(&c->bbuf, m2 * sizeof(double)));
   CK(cudaMalloc(&c->tbuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->phit, ncm * sizeof(double)));
-  CK(cudaMalloc(&c->phi, ncm * sizeof(double)));
   CK(cudaMalloc(&c->scal, 16 * sizeof(double)));
   CK(cudaMalloc(&c->red_part, RED_BLOCKS * sizeof(double)));
   CK(cudaMalloc(&c->red_cnt, sizeof(unsigned)));
   CK(cudaMemsetAsync(c->red_cnt, 0, sizeof(unsigned), c->stream));
   CK(cudaMalloc(&c->dflag, sizeof(int)));
   CK(cudaMallocHost(&c->host_info, 8 * sizeof(double)));
-  if (c->sharded) {
-    const int64_t st = std::max<int64_t>(2 * c->np, c->kp);
-    CK(cudaMalloc(&c->stage, st * sizeof(double)));
-    CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
-  }
 
   tr.mark("upload + buffers");
   // ---- launch geometry (global sizes only => P-invariant sums)
   c->chunk_mv = choose_chunk(n, n, MV_TPB * MV_T);
   c->nchunk_mv = cdiv(n, c->chunk_mv);
-  c->chunk_src = choose_chunk(n, std::max<int64_t>(nc, 1), SRC_TPB * SRC_T);
-  c->nchunk_src = cdiv(std::max<int64_t>(nc, 1), c->chunk_src);
-  c->chunk_en = choose_chunk(std::max<int64_t>(nc, 1), n, EN_TPB * EN_T);
-  c->nchunk_en = cdiv(n, c->chunk_en);
 
-  // ---- symmetric matvec schedule (bipb_sym.cuh): I-blocks sharded by rank
+  // ---- default matvec kernel: symmetric once there are >= 2 waves of (I, J) tiles, else the row
+  // kernel (small problems); BIPB_MATVEC=row|sym overrides.  Symmetric buffers are allocated on
+  // first use (sym_plan).
   {
-    c->sym_nb = cdiv(n, SYM_B);
-    c->sym_hmax = (c->sym_nb & 1) ? (c->sym_nb - 1) / 2 : c->sym_nb / 2;
-    bipb_partition(c->sym_nb, c->world, c->rank, &c->sym_I0, &c->sym_I1);
-    const int64_t tiles_local = (c->sym_I1 - c->sym_I0) * (c->sym_hmax + 1);
-    c->sym_W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / WANT_CTAS));
-    c->sym_runs = cdiv(c->sym_hmax + 1, c->sym_W);
-    // default kernel: symmetric once there are >= 2 waves of (I, J) tiles, else the row kernel
-    c->mv_kind = (c->sym_nb * (c->sym_hmax + 1) >= 2 * 2 * 148) ? 1 : 0;
+    const int64_t nb1 = cdiv(n, (int64_t)SymCfg<1>::TPB * SymCfg<1>::T);
+    const int64_t h1 = (nb1 & 1) ? (nb1 - 1) / 2 : nb1 / 2;
+    c->mv_kind = (nb1 * (h1 + 1) >= 2 * 2 * 148) ? 1 : 0;
     const char* env = getenv("BIPB_MATVEC");
     if (env && (!strcmp(env, "row") || !strcmp(env, "0"))) c->mv_kind = 0;
     if (env && (!strcmp(env, "sym") || !strcmp(env, "1"))) c->mv_kind = 1;
-    const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * SYM_REC;  // tile-SoA, padded to whole tiles
-    CK(cudaMalloc(&c->rec_sym, rec_doubles * sizeof(double)));
-    CK(cudaMemsetAsync(c->rec_sym, 0, rec_doubles * sizeof(double), c->stream));
-    const int64_t nbl = std::max<int64_t>(1, c->sym_I1 - c->sym_I0);  // partials only for this rank's I-blocks
-    CK(cudaMalloc(&c->sym_fwd, (size_t)nbl * c->sym_runs * 2 * SYM_B * sizeof(double)));
-    CK(cudaMalloc(&c->sym_rev, (size_t)nbl * (c->sym_hmax + 1) * 2 * SYM_B * sizeof(double)));
-    if (c->sharded) CK(cudaMalloc(&c->sym_p, (size_t)2 * n * sizeof(double)));
+    if (c->mv_kind == 1) {
+      bipb_ctx::SymPlan* p;
+      CKS(sym_plan<1>(c, &p));
+    }
   }
-
   tr.mark("symmetric-kernel buffers");
-  // ---- singular configuration: a charge within 1e-6 A of a centroid (R11)
-  if (nc > 0) {
-    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
-    std::vector<double> rx(n), ry(n), rz(n);
-    for (int64_t i = 0; i < n; ++i) { rx[i] = C[3 * i]; ry[i] = C[3 * i + 1]; rz[i] = C[3 * i + 2]; }
-    double *drx, *dry, *drz;
-    CKS(up(&drx, rx)); CKS(up(&dry, ry)); CKS(up(&drz, rz));
-    LAUNCH1D(min_dist_kernel, n, drx, dry, drz, n, c->q4, nc, 1e-12, c->dflag);
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    cudaFree(drx); cudaFree(dry); cudaFree(drz);
-    if (flag) return fail(BIPB_ERR_SINGULAR, "a charge lies within 1e-6 A of an element centroid");
-  }
-
+  // ---- charges (layout, sharding, chunking, singular check)
+  CKS(load_charges(c, nc, Q));
   tr.mark("singular check");
   // ---- NCCL communicator
   if (c->sharded && !c->no_comm) {
@@ -683,6 +759,32 @@ bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
   return BIPB_OK;
 }
 
+// Y = A U for nrhs operands (device, [nrhs][2n]); symmetric kernel in passes of 4, 2, 1 operands,
+// row kernel one by one.
+static bipb_status matvec_batch_dev(bipb_ctx* c, int nrhs, const double* U, double* Y) {
+  const int64_t m2 = 2 * c->n;
+  int done = 0;
+  while (done < nrhs) {
+    const int left = nrhs - done;
+    const double* u = U + (int64_t)done * m2;
+    double* y = Y + (int64_t)done * m2;
+    if (c->mv_kind == 0) {
+      CKS(matvec_dev(c, u, y));
+      done += 1;
+    } else if (left >= 4) {
+      CKS(matvec_sym_R<4>(c, u, y));
+      done += 4;
+    } else if (left >= 2) {
+      CKS(matvec_sym_R<2>(c, u, y));
+      done += 2;
+    } else {
+      CKS(matvec_sym_R<1>(c, u, y));
+      done += 1;
+    }
+  }
+  return BIPB_OK;
+}
+
 static bipb_status ensure_krylov(bipb_ctx* c, int m) {
   if (m <= c->m_cap) return BIPB_OK;
   double* bufs[] = {c->V, c->H, c->cs, c->sn, c->g, c->yk};
@@ -697,6 +799,192 @@ static bipb_status ensure_krylov(bipb_ctx* c, int m) {
   CK(cudaMalloc(&c->g, (size_t)(m + 1) * sizeof(double)));
   CK(cudaMalloc(&c->yk, (size_t)m * sizeof(double)));
   c->m_cap = m;
+  return BIPB_OK;
+}
+
+
+// ---- multi-RHS GMRES: nrhs independent GMRES(m) runs in lockstep,
+// each exactly the algorithm of bipb_gmres_solve; every Arnoldi step applies A to all systems
+// still iterating through one batched (shared-pair) product.
+struct GmresSys {
+  double *V = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *g = nullptr, *yk = nullptr, *S = nullptr;
+  const double* b = nullptr;
+  double* x = nullptr;
+  double beta_b = 0.0, rel = 1.0;
+  int64_t its = 0, restarts = 0, matvecs = 0, hl = 0;
+  int kdone = 0;
+  bool converged = false, finished = false, in_cycle = false, first = true;
+  bipb_report* rep = nullptr;
+};
+
+static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd, double* const* xd, int m, double tol,
+                                    int max_iters, int check_true, bipb_report* reps, int* n_not_conv) {
+  const int64_t m2 = 2 * c->n;
+  std::vector<GmresSys> sy(R);
+  std::vector<double*> owned;
+  auto alloc = [&](double** p, size_t cnt) -> bipb_status {
+    CK(cudaMalloc(p, cnt * sizeof(double)));
+    owned.push_back(*p);
+    return BIPB_OK;
+  };
+  struct Guard {
+    std::vector<double*>* v;
+    ~Guard() {
+      for (double* p : *v) cudaFree(p);
+    }
+  } guard{&owned};
+  double *U = nullptr, *Y = nullptr;
+  CKS(alloc(&U, (size_t)R * m2));
+  CKS(alloc(&Y, (size_t)R * m2));
+  for (int r = 0; r < R; ++r) {
+    GmresSys& q = sy[r];
+    q.b = bd[r];
+    q.x = xd[r];
+    q.rep = reps ? reps + r : nullptr;
+    CKS(alloc(&q.V, (size_t)(m + 1) * m2));
+    CKS(alloc(&q.H, (size_t)(m + 1) * m));
+    CKS(alloc(&q.cs, (size_t)m));
+    CKS(alloc(&q.sn, (size_t)m));
+    CKS(alloc(&q.g, (size_t)(m + 1)));
+    CKS(alloc(&q.yk, (size_t)m));
+    CKS(alloc(&q.S, 16));
+    CKS(dot_dev(c, q.b, q.b, m2, 1.0, q.S + 0));
+    LAUNCH1D(sqrt_kernel, 1, q.S + 0, q.S + 0);
+  }
+  double h2[2];
+  for (int r = 0; r < R; ++r) {
+    CKS(read_scalars(c, sy[r].S, 1, h2));
+    sy[r].beta_b = h2[0];
+    if (h2[0] == 0.0) {
+      CK(cudaMemsetAsync(sy[r].x, 0, m2 * sizeof(double), c->stream));
+      sy[r].converged = sy[r].finished = true;
+      sy[r].rel = 0.0;
+    }
+  }
+  // batched A applied to the listed systems' vectors src(q) -> dst(q)
+  auto apply = [&](std::vector<int>& list, auto src, auto dst) -> bipb_status {
+    const int k = (int)list.size();
+    if (k == 0) return BIPB_OK;
+    for (int t = 0; t < k; ++t)
+      CK(cudaMemcpyAsync(U + t * m2, src(sy[list[t]]), m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CKS(matvec_batch_dev(c, k, U, Y));
+    for (int t = 0; t < k; ++t) {
+      CK(cudaMemcpyAsync(dst(sy[list[t]]), Y + t * m2, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      sy[list[t]].matvecs++;
+    }
+    return BIPB_OK;
+  };
+  for (;;) {
+    // ---- cycle start: r = b - A x for every unfinished system (x = 0: r = b, no product)
+    std::vector<int> need, act;
+    for (int r = 0; r < R; ++r) {
+      GmresSys& q = sy[r];
+      if (q.finished) continue;
+      CKS(dot_dev(c, q.x, q.x, m2, 1.0, q.S + 4));
+      CKS(read_scalars(c, q.S + 4, 1, h2));
+      if (h2[0] == 0.0) {
+        CK(cudaMemcpyAsync(q.V, q.b, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      } else {
+        need.push_back(r);
+      }
+      act.push_back(r);
+    }
+    if (act.empty()) break;
+    CKS(apply(need, [](GmresSys& q) { return (const double*)q.x; }, [](GmresSys& q) { return q.V; }));
+    for (int r : need) LAUNCH1D(residual_kernel, m2, sy[r].V, sy[r].b, sy[r].V, m2);
+    std::vector<int> iter;
+    for (int r : act) {
+      GmresSys& q = sy[r];
+      if (!q.first) ++q.restarts;
+      q.first = false;
+      CKS(dot_dev(c, q.V, q.V, m2, 1.0, q.S + 1));
+      LAUNCH1D(sqrt_kernel, 1, q.S + 1, q.S + 1);
+      CKS(read_scalars(c, q.S + 1, 1, h2));
+      q.rel = h2[0] / q.beta_b;
+      if (q.rel <= tol) { q.converged = q.finished = true; continue; }
+      if (q.its >= max_iters) { q.finished = true; continue; }
+      LAUNCH1D(scale_div_kernel, m2, q.V, q.V, q.S + 1, m2);
+      init_g_kernel<<<1, 32, 0, c->stream>>>(q.g, q.S + 1, m);
+      c->launches_all++;
+      q.kdone = 0;
+      q.in_cycle = true;
+      iter.push_back(r);
+    }
+    // ---- Arnoldi steps in lockstep
+    for (int k = 0; k < m && !iter.empty(); ++k) {
+      CKS(apply(iter, [k, m2](GmresSys& q) { return (const double*)(q.V + (int64_t)k * m2); },
+                [k, m2](GmresSys& q) { return q.V + (int64_t)(k + 1) * m2; }));
+      std::vector<int> next;
+      for (int r : iter) {
+        GmresSys& q = sy[r];
+        q.its++;
+        double* w = q.V + (int64_t)(k + 1) * m2;
+        axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, nullptr, nullptr, q.V, m2, c->red_part,
+                                                                    c->red_cnt, q.H + k);
+        c->launches_all++;
+        for (int i = 0; i <= k; ++i) {
+          const double* zi = (i < k) ? q.V + (int64_t)(i + 1) * m2 : w;
+          double* outp = (i < k) ? q.H + (int64_t)(i + 1) * m + k : q.S + 2;
+          axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, q.V + (int64_t)i * m2, q.H + (int64_t)i * m + k,
+                                                                      zi, m2, c->red_part, c->red_cnt, outp);
+          c->launches_all++;
+        }
+        givens_kernel<<<1, 1, 0, c->stream>>>(q.H, q.cs, q.sn, q.g, q.S + 2, q.S + 3, k, m, q.beta_b, q.S + 6);
+        c->launches_all++;
+        CK(cudaGetLastError());
+        CKS(read_scalars(c, q.S + 6, 2, h2));
+        q.rel = h2[0];
+        if (q.rep && q.rep->history && q.hl < q.rep->history_cap) q.rep->history[q.hl] = q.rel;
+        ++q.hl;
+        q.kdone = k + 1;
+        if (h2[1] <= 1e-14 * q.beta_b) continue;  // happy breakdown: leaves the cycle
+        LAUNCH1D(scale_div_kernel, m2, w, w, q.S + 3, m2);
+        if (q.rel <= tol || q.its >= max_iters) continue;
+        next.push_back(r);
+      }
+      iter.swap(next);
+    }
+    // ---- end of cycle: x += V y for the systems that iterated
+    for (int r = 0; r < R; ++r) {
+      GmresSys& q = sy[r];
+      if (!q.in_cycle) continue;
+      q.in_cycle = false;
+      backsolve_kernel<<<1, 1, 0, c->stream>>>(q.H, q.g, q.yk, q.kdone, m);
+      c->launches_all++;
+      LAUNCH1D(update_x_kernel, m2, q.x, q.V, q.yk, q.kdone, m2);
+      if (q.rel <= tol) q.converged = q.finished = true;
+      else if (q.its >= max_iters) q.finished = true;
+    }
+  }
+  if (check_true) {
+    std::vector<int> all;
+    for (int r = 0; r < R; ++r)
+      if (sy[r].beta_b != 0.0) all.push_back(r);
+    CKS(apply(all, [](GmresSys& q) { return (const double*)q.x; }, [](GmresSys& q) { return q.V; }));
+    for (int r : all) {
+      GmresSys& q = sy[r];
+      LAUNCH1D(residual_kernel, m2, q.V, q.b, q.V, m2);
+      CKS(dot_dev(c, q.V, q.V, m2, 1.0, q.S + 4));
+      LAUNCH1D(sqrt_kernel, 1, q.S + 4, q.S + 4);
+      CKS(read_scalars(c, q.S + 4, 1, h2));
+      if (q.rep) q.rep->rel_res_true = h2[0] / q.beta_b;
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  *n_not_conv = 0;
+  for (int r = 0; r < R; ++r) {
+    GmresSys& q = sy[r];
+    if (!q.converged) ++*n_not_conv;
+    if (q.rep) {
+      q.rep->iterations = q.its;
+      q.rep->restarts = q.restarts;
+      q.rep->matvecs = q.matvecs;
+      q.rep->converged = q.converged ? 1 : 0;
+      q.rep->rel_res_est = q.rel;
+      q.rep->history_len = q.hl;
+      if (!check_true) q.rep->rel_res_true = (q.beta_b == 0.0) ? 0.0 : -1.0;
+    }
+  }
   return BIPB_OK;
 }
 
@@ -813,6 +1101,41 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
   return BIPB_OK;
 }
 
+
+bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, double* X, int32_t restart_m,
+                                   double tol, int32_t max_iters, int32_t check_true, bipb_report* reps) {
+  if (!c || !B || !X || nrhs < 1) return fail(BIPB_ERR_ARG, "NULL argument or nrhs < 1");
+  if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
+  const int64_t m2 = 2 * c->n;
+  const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
+  double *bst = nullptr, *xst = nullptr;
+  if (!bdev) {
+    CK(cudaMalloc(&bst, (size_t)nrhs * m2 * sizeof(double)));
+    CK(cudaMemcpyAsync(bst, B, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  if (!xdev) {
+    CK(cudaMalloc(&xst, (size_t)nrhs * m2 * sizeof(double)));
+    CK(cudaMemcpyAsync(xst, X, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  std::vector<const double*> bp(nrhs);
+  std::vector<double*> xp(nrhs);
+  for (int r = 0; r < nrhs; ++r) {
+    bp[r] = (bdev ? B : bst) + (int64_t)r * m2;
+    xp[r] = (xdev ? X : xst) + (int64_t)r * m2;
+  }
+  int not_conv = 0;
+  bipb_status st = gmres_batch_impl(c, nrhs, bp.data(), xp.data(), restart_m, tol, max_iters, check_true, reps,
+                                    &not_conv);
+  if (st == BIPB_OK && !xdev)
+    CK(cudaMemcpyAsync(X, xst, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  cudaStreamSynchronize(c->stream);
+  if (bst) cudaFree(bst);
+  if (xst) cudaFree(xst);
+  if (st != BIPB_OK) return st;
+  if (not_conv) return fail(BIPB_NOT_CONVERGED, std::to_string(not_conv) + " system(s) reached max_iters");
+  return BIPB_OK;
+}
+
 bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi_reac) {
   if (!c || !x || !e_sol) return fail(BIPB_ERR_ARG, "NULL argument");
   const int64_t n = c->n, nc = c->nc, m2 = 2 * n;
@@ -859,6 +1182,50 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
     }
   }
   CK(cudaMemcpyAsync(e_sol, &e, sizeof(double), cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double* Y) {
+  if (!c || !U || !Y || nrhs < 1) return fail(BIPB_ERR_ARG, "bad argument");
+  const int64_t m2 = 2 * c->n;
+  const bool udev = is_device_ptr(U), ydev = is_device_ptr(Y);
+  // host operands are staged through device buffers in slices of up to 4 operands
+  const int64_t slice = (udev && ydev) ? nrhs : 4;
+  if (!(udev && ydev) && !c->bat_U) {
+    CK(cudaMalloc(&c->bat_U, (size_t)4 * m2 * sizeof(double)));
+    CK(cudaMalloc(&c->bat_Y, (size_t)4 * m2 * sizeof(double)));
+  }
+  for (int64_t r0 = 0; r0 < nrhs; r0 += slice) {
+    const int k = (int)std::min<int64_t>(slice, nrhs - r0);
+    const double* ud = U + r0 * m2;
+    double* yd = Y + r0 * m2;
+    if (!udev) {
+      CK(cudaMemcpyAsync(c->bat_U, ud, (size_t)k * m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      ud = c->bat_U;
+    }
+    double* yk = ydev ? yd : c->bat_Y;
+    if (yk == ud) return fail(BIPB_ERR_ARG, "U and Y must not alias");
+    CKS(matvec_batch_dev(c, k, ud, yk));
+    if (!ydev) CK(cudaMemcpyAsync(yd, yk, (size_t)k * m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return BIPB_OK;
+}
+
+bipb_status bipb_set_charges(bipb_ctx* c, int64_t nc, const double* charges) {
+  if (!c || nc < 0 || (nc > 0 && !charges)) return fail(BIPB_ERR_ARG, "bad argument");
+  std::vector<double> Q(4 * std::max<int64_t>(nc, 0));
+  if (nc > 0) {
+    if (is_device_ptr(charges)) {
+      CK(cudaMemcpy(Q.data(), charges, Q.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      memcpy(Q.data(), charges, Q.size() * sizeof(double));
+    }
+  }
+  for (size_t k = 0; k < Q.size(); ++k)
+    if (!std::isfinite(Q[k])) return fail(BIPB_ERR_INPUT, "charge " + std::to_string(k / 4) + " not finite");
+  CKS(load_charges(c, nc, Q));
   CK(cudaStreamSynchronize(c->stream));
   return BIPB_OK;
 }

@@ -345,3 +345,70 @@ def test_symmetric_block_edges(bp, n_keep):
     ref = oracle.matvec(p, u)
     assert _rel(y, ref) <= 1e-11 and _rel(y0, ref) <= 1e-11
     ctx.close()
+
+
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 4, 7])
+@pytest.mark.parametrize("kappa", [g.KAPPA, 0.0])
+def test_matvec_batch(bp, nrhs, kappa):
+    """Multi-RHS product (passes of 4/2/1 operands sharing every pair evaluation) equals the
+    oracle for every operand, host and device buffers."""
+    import torch
+    p = g.sphere_problem(4, 4.0, np.zeros((0, 4)), kappa=kappa)
+    U = np.stack([g.random_vector(2 * p.n, 100 + r) for r in range(nrhs)])
+    ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(1)
+    Y = bp.bipb_matvec_batch(ctx, U)
+    for r in range(nrhs):
+        ref = oracle.matvec(p, U[r])
+        assert _rel(Y[r], ref) <= 1e-11
+        assert _rel(Y[r], bp.bipb_matvec(ctx, U[r])) <= 1e-14
+    Ud = torch.from_numpy(U).cuda()
+    Yd = torch.empty_like(Ud)
+    bp.bipb_matvec_batch(ctx, Ud, Yd)
+    assert _rel(Yd.cpu().numpy(), Y) <= 1e-15
+    ctx.set_matvec_kernel(0)  # row kernel loops
+    assert _rel(bp.bipb_matvec_batch(ctx, U), Y) <= 1e-14
+    ctx.close()
+
+
+def test_multi_rhs_charge_sets_and_batched_gmres(bp):
+    """Several charge sets on one surface (bipb_set_charges): source and energy parity per set,
+    and the lockstep multi-RHS GMRES equals the single-system solves (iterations, x, E)."""
+    p = g.sphere_problem(5, 4.0, g.charges_in_ball(50, 3.0, 2))  # C2 surface (symmetric kernel)
+    sets = [g.charges_in_ball(50, 3.0, s) for s in (2, 12, 13)] + [g.helix_charges()]
+    ctx = _ctx(bp, p)
+    assert ctx.matvec_kernel == 1
+    Bs, singles = [], []
+    for ch in sets:
+        bp.bipb_set_charges(ctx, ch)
+        q = g.Problem("set", p.centroids, p.normals, p.areas, ch, p.eps1, p.eps2, p.kappa)
+        b = bp.bipb_source(ctx)
+        rows = np.arange(0, p.n, 97)
+        sub = g.Problem("sub", p.centroids[rows], p.normals[rows], p.areas[rows], ch, p.eps1, p.eps2, p.kappa)
+        bo = oracle.source(sub)
+        np.testing.assert_allclose(b[rows], bo[:rows.size], rtol=1e-12)
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 300)
+        singles.append((x, rep, bp.bipb_energy(ctx, x)))
+        Bs.append(b)
+        xr = g.random_vector(2 * p.n, 7)
+        phi = np.zeros(len(ch))
+        bp.bipb_energy(ctx, xr, phi)
+        np.testing.assert_allclose(phi, oracle.reaction_potential(q, xr), rtol=1e-11, atol=1e-14 * np.abs(phi).max())
+    B = np.stack(Bs)
+    X = np.zeros_like(B)
+    st, reps = bp.bipb_gmres_solve_batch(ctx, B, X, 20, 1e-10, 300, check_true=True)
+    assert st == bp.OK
+    for r, ch in enumerate(sets):
+        xs, rs, es = singles[r]
+        assert abs(reps[r]["iterations"] - rs["iterations"]) <= 1
+        assert reps[r]["rel_res_true"] <= 1e-9
+        assert _rel(X[r], xs) <= 1e-9
+        bp.bipb_set_charges(ctx, ch)
+        assert bp.bipb_energy(ctx, X[r]) == pytest.approx(es, rel=1e-9)
+    # a singular charge set is rejected
+    bad = np.array([[*p.centroids[5], 1.0]])
+    with pytest.raises(bp.BipbError) as ei:
+        bp.bipb_set_charges(ctx, bad)
+    assert ei.value.status == bp.ERR_SINGULAR
+    ctx.close()

@@ -14,8 +14,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
 # symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb, pf, un in [(128, 4, 1, 1, 1), (128, 4, 3, 1, 1), (128, 4, 3, 0, 1), (64, 4, 6, 1, 1),
-                             (128, 4, 2, 1, 1)]:
+for tpb, t, minb, pf, un in [(128, 4, 1, 1, 1), (128, 4, 1, 2, 1), (128, 4, 1, 0, 1), (128, 3, 2, 2, 1)]:
     VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un})
 
 
@@ -92,6 +91,30 @@ if __name__ == "__main__":
             env = dict(os.environ, BIPB_MATVEC=kind)
             out = subprocess.run([sys.executable, __file__, "one", cfg, "3"], env=env, capture_output=True, text=True)
             print(kind, out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-800:], flush=True)
+    elif cmd == "batch":  # multi-RHS throughput of the default library: R operands per product
+        import numpy as np
+        import torch
+        import bipb_inputs as g
+        import paper_1301_5885_b200 as bp
+        cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
+        p = g.config(cfg)
+        ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa)
+        ctx.set_matvec_kernel(1)
+        for R in (1, 2, 4, 8):
+            U = torch.from_numpy(np.stack([g.random_vector(2 * p.n, r) for r in range(R)])).cuda()
+            Y = torch.empty_like(U)
+            bp.bipb_matvec_batch(ctx, U, Y)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(2):
+                bp.bipb_matvec_batch(ctx, U, Y)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / 2
+            print(json.dumps({"R": R, "ms_per_batch": ms, "pairs_per_s_all_rhs": R * p.n * (p.n - 1) / (ms / 1e3),
+                              "ms_per_rhs": ms / R}), flush=True)
+        ctx.close()
     elif cmd == "build":
         build()
     elif cmd == "one":
