@@ -183,3 +183,84 @@ def random_vector(n2: int, seed: int, smooth_centroids=None):
         f = np.cos(c[:, 0] * 0.3) + np.sin(0.2 * c[:, 1]) + 0.1 * c[:, 2]
         return np.ascontiguousarray(np.concatenate([f, 0.5 * f]))
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n2)
+
+
+# ---------------------------------------------------------------- molecular input formats
+# SURVEY.md §8(f) item 4 / SPEC.md S:49-84: the paper reads PDB/CHARMM22 charges and MSMS
+# triangulations.  These parsers ingest the text formats so real
+# molecular surfaces can be fed to bipb_setup; no molecular data ships with the repo.
+
+def parse_pqr(text: str) -> np.ndarray:
+    """PQR: records starting ATOM/HETATM; the last five whitespace-separated numeric fields
+    are x y z charge radius.  Returns [nc, 4] (x, y, z, Q) float64."""
+    rows = []
+    for ln, line in enumerate(text.splitlines(), 1):
+        if not (line.startswith("ATOM") or line.startswith("HETATM")):
+            continue
+        tok = line.split()
+        try:
+            x, y, z, q, r = (float(t) for t in tok[-5:])
+        except ValueError as e:
+            raise ValueError(f"PQR line {ln}: malformed numeric field") from e
+        rows.append((x, y, z, q))
+    if not rows:
+        raise ValueError("PQR: no ATOM/HETATM records")
+    return np.ascontiguousarray(np.array(rows, dtype=np.float64))
+
+
+def _data_lines(text: str):
+    lines = [l for l in text.splitlines() if l.strip()]
+    i = 0
+    while i < len(lines) and lines[i].lstrip().startswith("#"):
+        i += 1
+    return lines[i:]
+
+
+def parse_msms(vert_text: str, face_text: str):
+    """MSMS .vert/.face: after '#' comment lines and one counts line, vert
+    records begin 'x y z nx ny nz', face records begin 'i j k' (1-based).  Returns
+    (vertices [V,3], vertex_normals [V,3], faces [F,3] 0-based)."""
+    vl = _data_lines(vert_text)
+    fl = _data_lines(face_text)
+    nv = int(vl[0].split()[0])
+    nf = int(fl[0].split()[0])
+    V, VN = np.empty((nv, 3)), np.empty((nv, 3))
+    for k, l in enumerate(vl[1:1 + nv]):
+        t = l.split()
+        if len(t) < 6:
+            raise ValueError(f"MSMS vert record {k + 1}: fewer than 6 fields")
+        V[k] = [float(a) for a in t[:3]]
+        VN[k] = [float(a) for a in t[3:6]]
+    Fc = np.empty((nf, 3), dtype=np.int64)
+    for k, l in enumerate(fl[1:1 + nf]):
+        Fc[k] = [int(a) for a in l.split()[:3]]
+    if Fc.min() < 1 or Fc.max() > nv:
+        raise ValueError("MSMS face index out of range (indices are 1-based)")
+    return V, VN, Fc - 1
+
+
+def write_msms(vertices, vertex_normals, faces):
+    """Inverse of parse_msms (1-based faces), for fixtures and round trips."""
+    vt = ["# MSMS solvent excluded surface vertices", f"{len(vertices)} 0 0 0"]
+    vt += [" ".join(f"{a:.17g}" for a in (*v, *n)) + " 0 0 1" for v, n in zip(vertices, vertex_normals)]
+    ft = ["# MSMS solvent excluded surface faces", f"{len(faces)} 0 0 0"]
+    ft += [f"{a + 1} {b + 1} {c + 1} 1 1" for a, b, c in faces]
+    return "\n".join(vt) + "\n", "\n".join(ft) + "\n"
+
+
+def elements_from_msms(vertices, vertex_normals, faces, min_area=1e-12):
+    """Element precompute for an ingested mesh: centroid, unit normal from the
+    winding, flipped if it disagrees with the mean vertex normal; faces with area < min_area
+    are dropped.  Returns (centroids, normals, areas, n_dropped)."""
+    p0, p1, p2 = vertices[faces[:, 0]], vertices[faces[:, 1]], vertices[faces[:, 2]]
+    cr = np.cross(p1 - p0, p2 - p0)
+    nrm2 = np.linalg.norm(cr, axis=1)
+    area = 0.5 * nrm2
+    keep = area >= min_area
+    cen = (p0 + p1 + p2)[keep] / 3.0
+    nrm = cr[keep] / nrm2[keep, None]
+    vn = (vertex_normals[faces[:, 0]] + vertex_normals[faces[:, 1]] + vertex_normals[faces[:, 2]])[keep]
+    flip = np.einsum("ij,ij->i", nrm, vn) < 0
+    nrm[flip] *= -1.0
+    return (np.ascontiguousarray(cen), np.ascontiguousarray(nrm), np.ascontiguousarray(area[keep]),
+            int((~keep).sum()))

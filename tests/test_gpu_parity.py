@@ -412,3 +412,25 @@ def test_multi_rhs_charge_sets_and_batched_gmres(bp):
         bp.bipb_set_charges(ctx, bad)
     assert ei.value.status == bp.ERR_SINGULAR
     ctx.close()
+
+
+def test_ingested_msms_pqr_surface(bp):
+    """End to end on text inputs (§8(f) item 4): a bumpy star-shaped surface written and read
+    back in MSMS .vert/.face format with PQR charges, solved on the GPU vs the oracle."""
+    v, f = g.icosphere(3, 1.0)
+    u = v / np.linalg.norm(v, axis=1)[:, None]
+    rad = 6.0 + 0.6 * np.sin(3 * u[:, 0]) * np.cos(2 * u[:, 1]) + 0.4 * u[:, 2] ** 2
+    V0 = u * rad[:, None]
+    vert, face = g.write_msms(V0, u, f)
+    pqr = "".join(f"ATOM {k} C RES 1 {x:.6f} {y:.6f} {z:.6f} {q:.4f} 1.7\n"
+                  for k, (x, y, z, q) in enumerate(g.charges_in_ball(12, 3.5, 4)))
+    V, VN, F = g.parse_msms(vert, face)
+    c, nrm, a, dropped = g.elements_from_msms(V, VN, F)
+    p = g.Problem("msms", c, nrm, a, g.parse_pqr(pqr))
+    assert dropped == 0
+    ref = oracle.solve(p, restart=20, tol=1e-10)
+    ctx = _ctx(bp, p)
+    out = bp.solve(ctx, restart_m=20, tol=1e-10)
+    ctx.close()
+    assert abs(out["report"]["iterations"] - ref["report"]["iterations"]) <= 1
+    assert out["energy"] == pytest.approx(ref["energy"], rel=1e-8)
