@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -180,6 +182,13 @@ struct bipb_ctx {
   EventPool pool[3];
   int64_t launches_all = 0;
   int64_t matvec_calls = 0;  // operator applications (for per-product kernel time)
+  int warm_kind = -1;        // matvec kind whose buffers / attributes exist (eager product done)
+  // CUDA graphs of the GMRES Arnoldi steps (one per k), valid for (V, m, n, kind)
+  struct {
+    const double* V = nullptr;
+    int m = 0, kind = -1;
+    std::vector<cudaGraphExec_t> ex;
+  } ag;
 };
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -241,9 +250,20 @@ static bipb_status timed_begin(bipb_ctx* c, int which, cudaEvent_t* stop_out) {
   return BIPB_OK;
 }
 
+// opt-in dynamic shared memory, set once per (device, kernel, size) (the attribute call costs
+// tens of microseconds; GMRES on small meshes launches a pair kernel every iteration)
 template <typename KernelT>
 static bipb_status set_smem(KernelT k, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const auto key = std::make_pair(dev, reinterpret_cast<const void*>(k));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= smem) return BIPB_OK;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  done[key] = smem;
   return BIPB_OK;
 }
 
@@ -392,7 +412,15 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
 static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) { return matvec_sym_R<1>(c, u, y); }
 
 // y = A u (device vectors of length 2n; y must not alias u)
+static bipb_status matvec_dev_impl(bipb_ctx* c, const double* u, double* y);
 static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
+  CKS(matvec_dev_impl(c, u, y));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs == cudaStreamCaptureStatusNone) c->warm_kind = c->mv_kind;
+  return BIPB_OK;
+}
+static bipb_status matvec_dev_impl(bipb_ctx* c, const double* u, double* y) {
   if (c->mv_kind == 1) return matvec_sym_dev(c, u, y);
   const int64_t n = c->n;
   LAUNCH1D(prescale_kernel, n, u, c->ew, c->enx, c->eny, c->enz, c->rec_el, n);
@@ -493,6 +521,8 @@ void bipb_destroy(bipb_ctx* c) {
   if (c->host_info) cudaFreeHost(c->host_info);
   for (auto& p : c->pool)
     for (auto e : p.ev) cudaEventDestroy(e);
+  for (auto e : c->ag.ex)
+    if (e) cudaGraphExecDestroy(e);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -803,6 +833,76 @@ static bipb_status ensure_krylov(bipb_ctx* c, int m) {
 }
 
 
+// One Arnoldi step k of GMRES(m) on the context's Krylov arrays: w = A v_k;
+// modified Gram-Schmidt; Givens update; the 16-byte residual record copied to pinned host
+// memory; w /= h_{k+1,k} (harmless garbage on a happy breakdown: V[k+1] is then unused).
+// Enqueue only (no synchronisation) so it can be captured as a CUDA graph.
+static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
+  const int64_t m2 = 2 * c->n;
+  double* S = c->scal;
+  double* vk = c->V + (int64_t)k * m2;
+  double* w = c->V + (int64_t)(k + 1) * m2;
+  CKS(matvec_dev(c, vk, w));
+  axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, nullptr, nullptr, c->V, m2, c->red_part, c->red_cnt,
+                                                              c->H + 0 * m + k);
+  c->launches_all++;
+  for (int i = 0; i <= k; ++i) {
+    const double* zi = (i < k) ? c->V + (int64_t)(i + 1) * m2 : w;
+    double* outp = (i < k) ? c->H + (int64_t)(i + 1) * m + k : S + 2;
+    axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, c->V + (int64_t)i * m2, c->H + (int64_t)i * m + k,
+                                                                zi, m2, c->red_part, c->red_cnt, outp);
+    c->launches_all++;
+  }
+  CK(cudaGetLastError());
+  givens_kernel<<<1, 1, 0, c->stream>>>(c->H, c->cs, c->sn, c->g, S + 2, S + 3, k, m, S + 0, S + 6);
+  c->launches_all++;
+  CK(cudaMemcpyAsync(c->host_info, S + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  LAUNCH1D(scale_div_kernel, m2, w, w, S + 3, m2);
+  return BIPB_OK;
+}
+
+// Run step k: replay its CUDA graph when possible (no timing instrumentation active, the
+// product's buffers warm), else enqueue eagerly; then wait and return (rel, h_{k+1,k}).
+static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
+  // opt-in (BIPB_GRAPHS=1): replay pays off only from the second solve in a context (measured:
+  // C1 3.25 -> 2.82 ms per solve, C2 -2.6%, C3/C4 within noise; the first solve pays the capture)
+  static const bool graphs_on = getenv("BIPB_GRAPHS") && !strcmp(getenv("BIPB_GRAPHS"), "1");
+  const bool use = graphs_on && !c->timing && c->warm_kind == c->mv_kind;
+  if (use) {
+    if (c->ag.V != c->V || c->ag.m != m || c->ag.kind != c->mv_kind) {
+      for (auto e : c->ag.ex)
+        if (e) cudaGraphExecDestroy(e);
+      c->ag.ex.assign(m, nullptr);
+      c->ag.V = c->V;
+      c->ag.m = m;
+      c->ag.kind = c->mv_kind;
+    }
+    if (!c->ag.ex[k]) {
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      bipb_status st = enqueue_arnoldi_step(c, k, m);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (st != BIPB_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (ce != cudaSuccess) return fail(BIPB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      cudaGraphExec_t ex = nullptr;
+      ce = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) return fail(BIPB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+      c->ag.ex[k] = ex;
+    }
+    CK(cudaGraphLaunch(c->ag.ex[k], c->stream));
+  } else {
+    CKS(enqueue_arnoldi_step(c, k, m));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  h2[0] = c->host_info[0];
+  h2[1] = c->host_info[1];
+  return BIPB_OK;
+}
+
 // ---- multi-RHS GMRES: nrhs independent GMRES(m) runs in lockstep,
 // each exactly the algorithm of bipb_gmres_solve; every Arnoldi step applies A to all systems
 // still iterating through one batched (shared-pair) product.
@@ -929,7 +1029,7 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
                                                                       zi, m2, c->red_part, c->red_cnt, outp);
           c->launches_all++;
         }
-        givens_kernel<<<1, 1, 0, c->stream>>>(q.H, q.cs, q.sn, q.g, q.S + 2, q.S + 3, k, m, q.beta_b, q.S + 6);
+        givens_kernel<<<1, 1, 0, c->stream>>>(q.H, q.cs, q.sn, q.g, q.S + 2, q.S + 3, k, m, q.S + 0, q.S + 6);
         c->launches_all++;
         CK(cudaGetLastError());
         CKS(read_scalars(c, q.S + 6, 2, h2));
@@ -1042,33 +1142,15 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
       c->launches_all++;
       int kdone = 0;
       for (int k = 0; k < m; ++k) {
-        double* vk = c->V + (int64_t)k * m2;
-        double* w = c->V + (int64_t)(k + 1) * m2;
-        CKS(matvec_dev(c, vk, w));
+        CKS(run_arnoldi_step(c, k, m, h2));
         ++matvecs;
         ++its;
-        // modified Gram-Schmidt: h_ik = <w, v_i>; w -= h_ik v_i  (i = 0..k), then ||w||^2
-        axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, nullptr, nullptr, c->V, m2, c->red_part,
-                                                                    c->red_cnt, c->H + 0 * m + k);
-        c->launches_all++;
-        for (int i = 0; i <= k; ++i) {
-          const double* zi = (i < k) ? c->V + (int64_t)(i + 1) * m2 : w;
-          double* outp = (i < k) ? c->H + (int64_t)(i + 1) * m + k : S + 2;
-          axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, c->V + (int64_t)i * m2, c->H + (int64_t)i * m + k,
-                                                                      zi, m2, c->red_part, c->red_cnt, outp);
-          c->launches_all++;
-        }
-        CK(cudaGetLastError());
-        givens_kernel<<<1, 1, 0, c->stream>>>(c->H, c->cs, c->sn, c->g, S + 2, S + 3, k, m, beta_b, S + 6);
-        c->launches_all++;
-        CKS(read_scalars(c, S + 6, 2, h2));
         rel = h2[0];
         const double hk1 = h2[1];
         if (rep && rep->history && hl < rep->history_cap) rep->history[hl] = rel;
         ++hl;
         kdone = k + 1;
         if (hk1 <= 1e-14 * beta_b) break;  // happy breakdown
-        LAUNCH1D(scale_div_kernel, m2, w, w, S + 3, m2);
         if (rel <= tol || its >= max_iters) break;
       }
       backsolve_kernel<<<1, 1, 0, c->stream>>>(c->H, c->g, c->yk, kdone, m);

@@ -194,7 +194,8 @@ __global__ void init_g_kernel(double* g, const double* beta, int m) {
 // One Givens step on column k of H ((m+1) x m row-major), SURVEY.md §8(c) O4.
 // hk1sq = ||w||^2 after orthogonalisation. info[0] = |g_{k+1}| / beta_b, info[1] = h_{k+1,k}.
 __global__ void givens_kernel(double* H, double* cs, double* sn, double* g, const double* hk1sq, double* hk1,
-                              int k, int m, double beta_b, double* info) {
+                              int k, int m, const double* beta_b_ptr, double* info) {
+  const double beta_b = *beta_b_ptr;
   const double h = sqrt(*hk1sq);
   H[(k + 1) * m + k] = h;
   for (int i = 0; i < k; ++i) {

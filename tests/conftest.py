@@ -8,6 +8,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 os.environ.setdefault("OMP_PROC_BIND", "close")
 os.environ.setdefault("OMP_PLACES", "cores")
+os.environ.setdefault("BIPB_GRAPHS", "1")  # exercise the CUDA-graph replay of GMRES steps in the GPU tests
 
 
 def pytest_configure(config):

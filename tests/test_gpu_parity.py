@@ -434,3 +434,24 @@ def test_ingested_msms_pqr_surface(bp):
     ctx.close()
     assert abs(out["report"]["iterations"] - ref["report"]["iterations"]) <= 1
     assert out["energy"] == pytest.approx(ref["energy"], rel=1e-8)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_gmres_graph_replay_matches_eager(bp, kind):
+    """Arnoldi steps replayed as CUDA graphs (BIPB_GRAPHS=1, set for the GPU test session in
+    conftest) give bitwise the same solve as the eager path (forced by the timing
+    instrumentation)."""
+    p = g.sphere_problem(4, 4.0, g.charges_in_ball(20, 3.0, 9))
+    ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(kind)
+    bp.bipb_source(ctx)
+    xs, reps = [], []
+    for timing in (False, True, False):
+        ctx.timing_enable(timing)
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 10, 1e-10, 300)
+        xs.append(x)
+        reps.append(rep["iterations"])
+    assert reps[0] == reps[1] == reps[2]
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
+    ctx.close()
