@@ -91,28 +91,28 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
 };
-static NcclApi& nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    // reuse an already-loaded libnccl (torch's) when there is one
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names) {
-      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
-      if (api.h) break;
-    }
-    if (api.h) {
-      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
-      api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
-      api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
-      api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
-      api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
-      api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce && api.CommDestroy &&
-               api.GetErrorString;
-    }
+static NcclApi load_nccl() {
+  NcclApi api;
+  // reuse an already-loaded libnccl (torch's) when there is one
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
   }
+  if (api.h) {
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+    api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce && api.CommDestroy &&
+             api.GetErrorString;
+  }
+  return api;
+}
+static NcclApi& nccl() {
+  static NcclApi api = load_nccl();  // thread-safe one-time initialisation
   return api;
 }
 
@@ -225,7 +225,6 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-template <typename K>
 static void launch_1d_cfg(int64_t work, int& grid, int& block) {
   block = 256;
   grid = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(work, block)), 148 * 8);
@@ -303,7 +302,7 @@ static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
 #define LAUNCH1D(kern, work, ...)                                   \
   do {                                                              \
     int g_, b_;                                                     \
-    launch_1d_cfg<int>((work), g_, b_);                             \
+    launch_1d_cfg((work), g_, b_);                             \
     kern<<<g_, b_, 0, c->stream>>>(__VA_ARGS__);                    \
     c->launches_all++;                                              \
     CK(cudaGetLastError());                                         \
