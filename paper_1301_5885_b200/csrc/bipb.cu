@@ -343,7 +343,8 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   p.hmax = (p.nb & 1) ? (p.nb - 1) / 2 : p.nb / 2;
   bipb_partition(p.nb, c->world, c->rank, &p.I0, &p.I1);
   const int64_t tiles_local = (p.I1 - p.I0) * (p.hmax + 1);
-  p.W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / WANT_CTAS));
+  // runs of W offsets per CTA: >= 16 waves of resident CTAs (2 per SM) on this rank, W <= 16
+  p.W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / (148 * 2 * 16)));
   p.runs = cdiv(p.hmax + 1, p.W);
   double gb = 4.0;
   if (const char* e = getenv("BIPB_SYM_MEM_GB")) gb = std::max(0.001, atof(e));
