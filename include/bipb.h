@@ -188,8 +188,8 @@ bipb_status bipb_nccl_unique_id(unsigned char* out);
  *      (K1, K4 symmetric; K2/K3 exchange under d -> -d); 28 instead of 48 FP64
  *      instructions per ordered pair; deterministic for a fixed rank count; across ranks
  *      the partial products are summed with ncclAllReduce.
- * Default: 1 when the problem has at least two waves of 512 x 512 tile pairs
- * (N >~ 11k), else 0.  BIPB_MATVEC=row|sym in the environment overrides it at setup.
+ * Default: 1 when the problem has at least one wave (296) of 640 x 640 tile pairs
+ * (N >~ 15k), else 0.  BIPB_MATVEC=row|sym in the environment overrides it at setup.
  */
 bipb_status bipb_set_matvec_kernel(bipb_ctx* ctx, int32_t kind);
 int32_t bipb_get_matvec_kernel(bipb_ctx* ctx);

@@ -38,7 +38,7 @@ constexpr int MV_TPB = BIPB_MV_TPB, MV_T = BIPB_MV_T, MV_MINB = BIPB_MV_MINB;
 #define BIPB_SYM_TPB 128
 #endif
 #ifndef BIPB_SYM_T
-#define BIPB_SYM_T 4
+#define BIPB_SYM_T 5
 #endif
 #ifndef BIPB_SYM_MINB
 #define BIPB_SYM_MINB 1
@@ -290,11 +290,35 @@ static bipb_status launch_pair(bipb_ctx* c, const PairArgs& a, int64_t nchunk, i
   return BIPB_OK;
 }
 
+// Device memory comes from the device's default stream-ordered pool, configured to retain freed
+// memory (release threshold = max): contexts created and destroyed per solve (the e2e path)
+// then neither pay cudaMalloc nor the occasional multi-100-ms cudaFree trim of large blocks.
+static void pool_init_once(int dev) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done.push_back(dev);
+}
+template <typename T>
+static cudaError_t dmalloc(bipb_ctx* c, T** p, size_t bytes) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, c->stream);
+}
+static void dfree(bipb_ctx* c, void* p) {
+  if (p) cudaFreeAsync(p, c->stream);
+}
+
 static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
   if (doubles <= c->part_cap) return BIPB_OK;
-  if (c->part) cudaFree(c->part);
+  if (c->part) dfree(c, c->part);
   c->part = nullptr;
-  CK(cudaMalloc(&c->part, doubles * sizeof(double)));
+  CK(dmalloc(c, &c->part, doubles * sizeof(double)));
   c->part_cap = doubles;
   return BIPB_OK;
 }
@@ -351,11 +375,11 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   const double per_block = (double)((p.hmax + 1) + p.runs) * R * 2 * B * sizeof(double);
   p.group = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(p.I1 - p.I0, 1), (int64_t)(gb * 1e9 / per_block)));
   const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * F;  // tile-SoA, padded to whole tiles
-  CK(cudaMalloc(&p.rec, rec_doubles * sizeof(double)));
+  CK(dmalloc(c, &p.rec, rec_doubles * sizeof(double)));
   CK(cudaMemsetAsync(p.rec, 0, rec_doubles * sizeof(double), c->stream));
-  CK(cudaMalloc(&p.fwd, (size_t)p.group * p.runs * R * 2 * B * sizeof(double)));
-  CK(cudaMalloc(&p.rev, (size_t)p.group * (p.hmax + 1) * R * 2 * B * sizeof(double)));
-  if (!c->sym_P) CK(cudaMalloc(&c->sym_P, (size_t)4 * 2 * n * sizeof(double)));
+  CK(dmalloc(c, &p.fwd, (size_t)p.group * p.runs * R * 2 * B * sizeof(double)));
+  CK(dmalloc(c, &p.rev, (size_t)p.group * (p.hmax + 1) * R * 2 * B * sizeof(double)));
+  if (!c->sym_P) CK(dmalloc(c, &c->sym_P, (size_t)4 * 2 * n * sizeof(double)));
   p.R = R;
   return BIPB_OK;
 }
@@ -510,20 +534,21 @@ void bipb_destroy(bipb_ctx* c) {
                     c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part,
                     c->sym_P, c->bat_U, c->bat_Y};
   for (double* p : bufs)
-    if (p) cudaFree(p);
+    if (p) dfree(c, p);
   for (auto& sp : c->sym) {
-    if (sp.rec) cudaFree(sp.rec);
-    if (sp.fwd) cudaFree(sp.fwd);
-    if (sp.rev) cudaFree(sp.rev);
+    if (sp.rec) dfree(c, sp.rec);
+    if (sp.fwd) dfree(c, sp.fwd);
+    if (sp.rev) dfree(c, sp.rev);
   }
-  if (c->red_cnt) cudaFree(c->red_cnt);
-  if (c->dflag) cudaFree(c->dflag);
+  if (c->red_cnt) dfree(c, c->red_cnt);
+  if (c->dflag) dfree(c, c->dflag);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (auto& p : c->pool)
     for (auto e : p.ev) cudaEventDestroy(e);
   for (auto e : c->ag.ex)
     if (e) cudaGraphExecDestroy(e);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->stream) cudaStreamSynchronize(c->stream);  // the stream-ordered frees have completed
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -533,7 +558,7 @@ void bipb_destroy(bipb_ctx* c) {
 static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<double>& Q) {
   double* olds[] = {c->qx, c->qy, c->qz, c->rec_ch, c->q4, c->phit, c->phi};
   for (double* p : olds)
-    if (p) cudaFree(p);
+    if (p) dfree(c, p);
   c->qx = c->qy = c->qz = c->rec_ch = c->q4 = c->phit = c->phi = nullptr;
   const int64_t ncm = std::max<int64_t>(nc, 1);
   std::vector<double> qxs(ncm, 0.0), qys(ncm, 0.0), qzs(ncm, 0.0), qrec(4 * ncm, 0.0), q4(4 * ncm, 0.0);
@@ -543,14 +568,14 @@ static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<doubl
     for (int d = 0; d < 4; ++d) q4[4 * k + d] = Q[4 * k + d];
   }
   auto up = [&](double** d, const std::vector<double>& h) -> bipb_status {
-    CK(cudaMalloc(d, h.size() * sizeof(double)));
+    CK(dmalloc(c, d, h.size() * sizeof(double)));
     CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     return BIPB_OK;
   };
   CKS(up(&c->qx, qxs)); CKS(up(&c->qy, qys)); CKS(up(&c->qz, qzs));
   CKS(up(&c->rec_ch, qrec)); CKS(up(&c->q4, q4));
-  CK(cudaMalloc(&c->phit, ncm * sizeof(double)));
-  CK(cudaMalloc(&c->phi, ncm * sizeof(double)));
+  CK(dmalloc(c, &c->phit, ncm * sizeof(double)));
+  CK(dmalloc(c, &c->phi, ncm * sizeof(double)));
   c->nc = nc;
   c->have_b = false;
   bipb_partition(nc, c->world, c->rank, &c->k0, &c->k1);
@@ -558,11 +583,11 @@ static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<doubl
   if (c->sharded) {
     const int64_t st = std::max<int64_t>(2 * c->np, c->kp);
     if (st > c->stage_cap) {
-      if (c->stage) cudaFree(c->stage);
-      if (c->gather) cudaFree(c->gather);
+      if (c->stage) dfree(c, c->stage);
+      if (c->gather) dfree(c, c->gather);
       c->stage = c->gather = nullptr;
-      CK(cudaMalloc(&c->stage, st * sizeof(double)));
-      CK(cudaMalloc(&c->gather, (size_t)c->world * st * sizeof(double)));
+      CK(dmalloc(c, &c->stage, st * sizeof(double)));
+      CK(dmalloc(c, &c->gather, (size_t)c->world * st * sizeof(double)));
       c->stage_cap = st;
     }
   }
@@ -601,6 +626,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     if (dist->device >= 0) CK(cudaSetDevice(dist->device));
   }
   CK(cudaGetDevice(&c->device));
+  pool_init_once(c->device);
   CKS(fetch(centroids, C.data(), 3 * n));
   CKS(fetch(normals, Nn.data(), 3 * n));
   CKS(fetch(areas, W.data(), n));
@@ -656,7 +682,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     for (int d = 3; d < 8; ++d) rec[8 * i + d] = 0.0;
   }
   auto up = [&](double** d, const std::vector<double>& h) -> bipb_status {
-    CK(cudaMalloc(d, h.size() * sizeof(double)));
+    CK(dmalloc(c, d, h.size() * sizeof(double)));
     CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     return BIPB_OK;
   };
@@ -664,17 +690,17 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   CKS(up(&c->enx, nx)); CKS(up(&c->eny, ny)); CKS(up(&c->enz, nz));
   CKS(up(&c->ew, W)); CKS(up(&c->rec_el, rec));
   const int64_t m2 = 2 * n;
-  CK(cudaMalloc(&c->b, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->ubuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->ybuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->xbuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->bbuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->tbuf, m2 * sizeof(double)));
-  CK(cudaMalloc(&c->scal, 16 * sizeof(double)));
-  CK(cudaMalloc(&c->red_part, RED_BLOCKS * sizeof(double)));
-  CK(cudaMalloc(&c->red_cnt, sizeof(unsigned)));
+  CK(dmalloc(c, &c->b, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->ubuf, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->ybuf, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->xbuf, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->bbuf, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->tbuf, m2 * sizeof(double)));
+  CK(dmalloc(c, &c->scal, 16 * sizeof(double)));
+  CK(dmalloc(c, &c->red_part, RED_BLOCKS * sizeof(double)));
+  CK(dmalloc(c, &c->red_cnt, sizeof(unsigned)));
   CK(cudaMemsetAsync(c->red_cnt, 0, sizeof(unsigned), c->stream));
-  CK(cudaMalloc(&c->dflag, sizeof(int)));
+  CK(dmalloc(c, &c->dflag, sizeof(int)));
   CK(cudaMallocHost(&c->host_info, 8 * sizeof(double)));
 
   tr.mark("upload + buffers");
@@ -682,13 +708,14 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->chunk_mv = choose_chunk(n, n, MV_TPB * MV_T);
   c->nchunk_mv = cdiv(n, c->chunk_mv);
 
-  // ---- default matvec kernel: symmetric once there are >= 2 waves of (I, J) tiles, else the row
+  // ---- default matvec kernel: symmetric once there is >= 1 wave of (I, J) tiles, else the row
   // kernel (small problems); BIPB_MATVEC=row|sym overrides.  Symmetric buffers are allocated on
   // first use (sym_plan).
   {
     const int64_t nb1 = cdiv(n, (int64_t)SymCfg<1>::TPB * SymCfg<1>::T);
     const int64_t h1 = (nb1 & 1) ? (nb1 - 1) / 2 : nb1 / 2;
-    c->mv_kind = (nb1 * (h1 + 1) >= 2 * 2 * 148) ? 1 : 0;
+    c->mv_kind = (nb1 * (h1 + 1) >= 2 * 148) ? 1 : 0;  // measured: C1 (40 tiles) row 0.13 ms vs sym 0.34;
+                                                       // C2 (544 tiles) sym 0.98 ms vs row 1.45
     const char* env = getenv("BIPB_MATVEC");
     if (env && (!strcmp(env, "row") || !strcmp(env, "0"))) c->mv_kind = 0;
     if (env && (!strcmp(env, "sym") || !strcmp(env, "1"))) c->mv_kind = 1;
@@ -819,15 +846,15 @@ static bipb_status ensure_krylov(bipb_ctx* c, int m) {
   if (m <= c->m_cap) return BIPB_OK;
   double* bufs[] = {c->V, c->H, c->cs, c->sn, c->g, c->yk};
   for (double* p : bufs)
-    if (p) cudaFree(p);
+    if (p) dfree(c, p);
   c->V = c->H = c->cs = c->sn = c->g = c->yk = nullptr;
   c->m_cap = 0;
-  CK(cudaMalloc(&c->V, (size_t)(m + 1) * 2 * c->n * sizeof(double)));
-  CK(cudaMalloc(&c->H, (size_t)(m + 1) * m * sizeof(double)));
-  CK(cudaMalloc(&c->cs, (size_t)m * sizeof(double)));
-  CK(cudaMalloc(&c->sn, (size_t)m * sizeof(double)));
-  CK(cudaMalloc(&c->g, (size_t)(m + 1) * sizeof(double)));
-  CK(cudaMalloc(&c->yk, (size_t)m * sizeof(double)));
+  CK(dmalloc(c, &c->V, (size_t)(m + 1) * 2 * c->n * sizeof(double)));
+  CK(dmalloc(c, &c->H, (size_t)(m + 1) * m * sizeof(double)));
+  CK(dmalloc(c, &c->cs, (size_t)m * sizeof(double)));
+  CK(dmalloc(c, &c->sn, (size_t)m * sizeof(double)));
+  CK(dmalloc(c, &c->g, (size_t)(m + 1) * sizeof(double)));
+  CK(dmalloc(c, &c->yk, (size_t)m * sizeof(double)));
   c->m_cap = m;
   return BIPB_OK;
 }
@@ -923,16 +950,17 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
   std::vector<GmresSys> sy(R);
   std::vector<double*> owned;
   auto alloc = [&](double** p, size_t cnt) -> bipb_status {
-    CK(cudaMalloc(p, cnt * sizeof(double)));
+    CK(dmalloc(c, p, cnt * sizeof(double)));
     owned.push_back(*p);
     return BIPB_OK;
   };
   struct Guard {
+    bipb_ctx* c;
     std::vector<double*>* v;
     ~Guard() {
-      for (double* p : *v) cudaFree(p);
+      for (double* p : *v) dfree(c, p);
     }
-  } guard{&owned};
+  } guard{c, &owned};
   double *U = nullptr, *Y = nullptr;
   CKS(alloc(&U, (size_t)R * m2));
   CKS(alloc(&Y, (size_t)R * m2));
@@ -1192,11 +1220,11 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
   const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
   double *bst = nullptr, *xst = nullptr;
   if (!bdev) {
-    CK(cudaMalloc(&bst, (size_t)nrhs * m2 * sizeof(double)));
+    CK(dmalloc(c, &bst, (size_t)nrhs * m2 * sizeof(double)));
     CK(cudaMemcpyAsync(bst, B, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
   if (!xdev) {
-    CK(cudaMalloc(&xst, (size_t)nrhs * m2 * sizeof(double)));
+    CK(dmalloc(c, &xst, (size_t)nrhs * m2 * sizeof(double)));
     CK(cudaMemcpyAsync(xst, X, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
   std::vector<const double*> bp(nrhs);
@@ -1211,8 +1239,8 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
   if (st == BIPB_OK && !xdev)
     CK(cudaMemcpyAsync(X, xst, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   cudaStreamSynchronize(c->stream);
-  if (bst) cudaFree(bst);
-  if (xst) cudaFree(xst);
+  if (bst) dfree(c, bst);
+  if (xst) dfree(c, xst);
   if (st != BIPB_OK) return st;
   if (not_conv) return fail(BIPB_NOT_CONVERGED, std::to_string(not_conv) + " system(s) reached max_iters");
   return BIPB_OK;
@@ -1275,8 +1303,8 @@ bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double
   // host operands are staged through device buffers in slices of up to 4 operands
   const int64_t slice = (udev && ydev) ? nrhs : 4;
   if (!(udev && ydev) && !c->bat_U) {
-    CK(cudaMalloc(&c->bat_U, (size_t)4 * m2 * sizeof(double)));
-    CK(cudaMalloc(&c->bat_Y, (size_t)4 * m2 * sizeof(double)));
+    CK(dmalloc(c, &c->bat_U, (size_t)4 * m2 * sizeof(double)));
+    CK(dmalloc(c, &c->bat_Y, (size_t)4 * m2 * sizeof(double)));
   }
   for (int64_t r0 = 0; r0 < nrhs; r0 += slice) {
     const int k = (int)std::min<int64_t>(slice, nrhs - r0);

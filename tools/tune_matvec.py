@@ -14,7 +14,8 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
 # symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb, pf, un in [(128, 4, 1, 1, 1), (128, 4, 1, 2, 1), (128, 4, 1, 0, 1), (128, 3, 2, 2, 1)]:
+for tpb, t, minb, pf, un in [(128, 4, 1, 1, 1), (128, 5, 1, 1, 1), (96, 4, 2, 1, 1), (160, 4, 1, 1, 1),
+                             (128, 5, 1, 0, 1)]:
     VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un})
 
 
