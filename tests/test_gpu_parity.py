@@ -455,3 +455,21 @@ def test_gmres_graph_replay_matches_eager(bp, kind):
     assert reps[0] == reps[1] == reps[2]
     assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
     ctx.close()
+
+
+def test_full_size_c5_sampled_matvec(bp):
+    """C5 (N = 1,310,720; partials launched in I-block groups): sampled rows of one product
+    against the oracle, and the symmetric and row kernels against each other."""
+    p = g.config("C5")
+    ctx = _ctx(bp, p)
+    assert ctx.matvec_kernel == 1
+    u = g.random_vector(2 * p.n, 31)
+    y = bp.bipb_matvec(ctx, u)
+    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 12).astype(np.int64), [0, 639, 640, p.n - 1]]))
+    yi, yin = oracle.matvec_rows(p, u, rows)
+    assert np.max(np.abs(y[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
+    assert np.max(np.abs(y[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))
+    ctx.set_matvec_kernel(0)
+    y0 = bp.bipb_matvec(ctx, u)
+    assert _rel(y, y0) <= 1e-13
+    ctx.close()
