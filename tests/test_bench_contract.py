@@ -1,0 +1,39 @@
+"""bench.py contract: the JSON line carries the keys the driver reads (reference arm on CPU;
+native arm on the GPU)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REQUIRED = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches"}
+
+
+def _run(args, timeout):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    return json.loads(lines[0])
+
+
+def test_reference_arm_json():
+    d = _run(["--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "0"], 300)
+    assert REQUIRED <= set(d) and d["impl"] == "reference"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0 and d["gpu_launches"] == 0
+
+
+@pytest.mark.gpu
+def test_native_arm_json():
+    d = _run(["--config", "C2", "--steps", "1", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "2"], 900)
+    assert REQUIRED <= set(d) and d["metric"] == "fp64_pair_interactions_per_sec"
+    r = d["roofline"]
+    assert r["bound"] == "alu" and 0 < r["frac"] < 1.5 and r["peak"] > 30
+    assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert d["cpu_baseline"]["kind"] == "oracle"
