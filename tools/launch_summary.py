@@ -2,7 +2,10 @@
 launches, summed device time, share.  Usage: python tools/launch_summary.py launches.csv"""
 import collections
 import csv
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 hdr = rows[0]
