@@ -93,11 +93,13 @@ struct NcclApi {
 };
 static NcclApi load_nccl() {
   NcclApi api;
+  // BIPB_NCCL_LIB: explicit library (tests use a one-GPU stand-in, tests/fakenccl); otherwise
   // reuse an already-loaded libnccl (torch's) when there is one
+  if (const char* lib = getenv("BIPB_NCCL_LIB")) api.h = dlopen(lib, RTLD_NOW | RTLD_LOCAL);
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
-    api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
     if (api.h) break;
+    api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
   }
   if (api.h) {
     api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");

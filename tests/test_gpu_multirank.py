@@ -1,0 +1,82 @@
+"""The multi-rank code path on one GPU: 2 and 3 processes share the device and exchange through
+a test stand-in for NCCL (tests/fakenccl, selected with BIPB_NCCL_LIB; real NCCL refuses two
+ranks on one device).  Every rank runs the full pipeline (source -> replicated GMRES with one
+collective per product -> energy) and must reproduce the single-GPU results: bitwise for the
+row kernel (rank-count invariant sums), to rounding for the symmetric kernel (all-reduce of
+partial sums)."""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+import bipb_inputs as g
+
+pytestmark = pytest.mark.gpu
+FAKE = os.path.join(os.path.dirname(__file__), "fakenccl", "libfakenccl.so")
+
+
+def _problem():
+    return g.sphere_problem(5, 4.0, g.charges_in_ball(30, 3.0, 17))  # N = 20480 (symmetric default)
+
+
+def _run(rank, world, uid, kind, q):
+    os.environ["BIPB_NCCL_LIB"] = FAKE
+    os.environ["BIPB_GRAPHS"] = "0"  # the stand-in synchronises inside collectives: not capturable
+    try:
+        import paper_1301_5885_b200 as bp
+        p = _problem()
+        dist = None if world == 0 else (rank, world, uid, 0)
+        ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
+        ctx.set_matvec_kernel(kind)
+        u = g.random_vector(2 * p.n, 5)
+        y = bp.bipb_matvec(ctx, u)
+        Y = bp.bipb_matvec_batch(ctx, np.stack([u, 2 * u, -u]))
+        b = bp.bipb_source(ctx)
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 300)
+        phi = np.zeros(p.nc)
+        e = bp.bipb_energy(ctx, x, phi)
+        ctx.close()
+        q.put((rank, {"y": y, "Y": Y, "b": b, "x": x, "its": rep["iterations"], "e": e, "phi": phi}, None))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, None, repr(ex)))
+
+
+def _spawn(world, kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    uid = None
+    if world:
+        os.environ["BIPB_NCCL_LIB"] = FAKE
+        import paper_1301_5885_b200 as bp
+        uid = bp.bipb_nccl_unique_id()
+    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, q)) for r in range(max(world, 1))]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for _, _, err in res:
+        assert err is None, err
+    return [r[1] for r in sorted(res, key=lambda t: t[0])]
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_matches_single(world, kind):
+    assert os.path.exists(FAKE), "build tests/fakenccl/libfakenccl.so (__graft_entry__.build())"
+    ref = _spawn(0, kind)[0]
+    outs = _spawn(world, kind)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    for o in outs:  # every rank holds the full, identical result
+        assert np.array_equal(o["x"], outs[0]["x"]) and o["e"] == outs[0]["e"]
+        assert o["its"] == ref["its"]
+        if kind == 0:
+            assert np.array_equal(o["y"], ref["y"]) and np.array_equal(o["b"], ref["b"])
+            assert np.array_equal(o["x"], ref["x"]) and o["e"] == ref["e"]
+        else:
+            assert rel(o["y"], ref["y"]) <= 1e-14 and rel(o["Y"], ref["Y"]) <= 1e-14
+            assert np.array_equal(o["b"], ref["b"])
+            assert rel(o["x"], ref["x"]) <= 1e-11 and o["e"] == pytest.approx(ref["e"], rel=1e-12)
+        np.testing.assert_allclose(o["phi"], ref["phi"], rtol=1e-13, atol=1e-16)
