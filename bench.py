@@ -179,10 +179,17 @@ def run_native(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         args.gpus = world
+    ndev = max(torch.cuda.device_count(), 1)
+    local = local % ndev  # BIPB_BENCH_PG=gloo + BIPB_NCCL_LIB=<stand-in>: several ranks on one GPU (tests)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    pg_backend = os.environ.get("BIPB_BENCH_PG", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if pg_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(pg_backend)
+    red_dev = dev if pg_backend == "nccl" else None
     prob = g.config(args.config)
     n, nc = prob.n, prob.nc
     from paper_1301_5885_b200 import dist as bd
@@ -240,7 +247,7 @@ def run_native(args):
     en_ms, _ = ctx.timing_get(2)
     _, all_launches = ctx.timing_get(3)
     ctx.timing_enable(False)
-    total_ms = bd.max_over_ranks(total_ms, world, dev)
+    total_ms = bd.max_over_ranks(total_ms, world, red_dev)
     matvecs = [r["matvecs"] for r in reps]
     pairs_per_step = [mv * n * (n - 1) + 2 * n * nc for mv in matvecs]
     value = sum(pairs_per_step) / (total_ms / 1e3)
@@ -325,7 +332,7 @@ def run_native(args):
             times.append(time.perf_counter() - t)
             pairs += rep["matvecs"] * n * (n - 1) + 2 * n * nc
         tsum = sum(times)
-        tsum = bd.max_over_ranks(tsum, world, dev)
+        tsum = bd.max_over_ranks(tsum, world, red_dev)
         line["e2e"] = {"value": pairs / tsum, "unit": UNIT, "h2d_bytes_per_step": 8 * (7 * n + 4 * nc + 2 * n),
                        "d2h_bytes_per_step": 8 * (2 * n + 1), "ms_per_step": 1e3 * tsum / ke, "steps": ke,
                        "phase_ms_per_step": {k: v / ke for k, v in phases.items()},

@@ -37,3 +37,20 @@ def test_native_arm_json():
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.gpu
+def test_native_arm_two_ranks_one_gpu():
+    """The torchrun launch the driver uses for N > 1, with two ranks sharing this GPU (gloo for
+    torch.distributed, the NCCL stand-in for the library's collectives)."""
+    fake = os.path.join(ROOT, "tests", "fakenccl", "libfakenccl.so")
+    env = dict(os.environ, BIPB_BENCH_PG="gloo", BIPB_NCCL_LIB=fake, BIPB_GRAPHS="0")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "1", "--warmup", "1", "--config", "C2", "--e2e-steps", "1"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert REQUIRED <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "strong" and "cpu_baseline" not in d
