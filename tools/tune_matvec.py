@@ -14,13 +14,16 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
 # symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb, pf, un in [(128, 4, 1, 1, 1), (128, 5, 1, 1, 1), (96, 4, 2, 1, 1), (160, 4, 1, 1, 1),
-                             (128, 5, 1, 0, 1)]:
-    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un})
+for tpb, t, minb, pf, un, tile, stages in [(128, 5, 1, 1, 1, 128, 3), (128, 5, 1, 1, 1, 128, 2),
+                                           (128, 5, 1, 1, 1, 128, 4), (128, 5, 1, 1, 1, 64, 4),
+                                           (128, 4, 1, 1, 1, 256, 2), (128, 5, 1, 1, 1, 32, 6)]:
+    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un,
+                     "tile": tile, "stages": stages})
 
 
 def name(v):
-    return f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}_un{v.get('un', 1)}"
+    return (f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}"
+            f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}")
 
 
 def build():
@@ -34,7 +37,8 @@ def build():
         if v.get("kind") == "sym":
             extra = [f"-DBIPB_SYM_TPB={v['tpb']}", f"-DBIPB_SYM_T={v['t']}", f"-DBIPB_SYM_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}", f"-DBIPB_SYM_PREFETCH={v.get('pf', 0)}",
-                     f"-DBIPB_SYM_UNROLL={v.get('un', 1)}"]
+                     f"-DBIPB_SYM_UNROLL={v.get('un', 1)}", f"-DBIPB_TILE={v.get('tile', 128)}",
+                     f"-DBIPB_STAGES={v.get('stages', 3)}"]
         else:
             extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}"]
