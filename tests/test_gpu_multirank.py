@@ -47,10 +47,10 @@ def _spawn(world, kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     uid = None
-    if world:
-        os.environ["BIPB_NCCL_LIB"] = FAKE
-        import paper_1301_5885_b200 as bp
-        uid = bp.bipb_nccl_unique_id()
+    if world:  # the stand-in's unique id is a shared-memory name (made here: the parent process
+        # must not load the stand-in into its own copy of the library)
+        import time
+        uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
     procs = [ctx.Process(target=_run, args=(r, world, uid, kind, q)) for r in range(max(world, 1))]
     for pr in procs:
         pr.start()
