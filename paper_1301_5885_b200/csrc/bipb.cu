@@ -653,7 +653,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   {  // exp table T[j] = 2^(-j/2^B), correctly rounded on the host (long double)
     double tab[EXP_TAB];
     for (int j = 0; j < EXP_TAB; ++j) tab[j] = (double)exp2l(-(long double)j / EXP_TAB);
-    CK(cudaMemcpyToSymbol(c_exp_tab, tab, sizeof(tab)));
+    CK(cudaMemcpyToSymbol(g_exp_tab, tab, sizeof(tab)));
   }
   tr.mark("fetch + validate");
   c->n = n; c->nc = nc; c->eps1 = eps1; c->eps2 = eps2; c->kappa = kappa;

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   double* sbuf = reinterpret_cast<double*>(smem_raw);  // [STAGES][F][TILE]
   double* rsum = sbuf + STAGES * TILE * F;              // [NW][R][2][B] per-warp reverse sums of the J-block
   uint64_t* full = reinterpret_cast<uint64_t*>(rsum + NW * R * 2 * B);
-  for (int i = threadIdx.x; i < EXP_TAB; i += TPB) s_tab[i] = c_exp_tab[i];
+  for (int i = threadIdx.x; i < EXP_TAB; i += TPB) s_tab[i] = g_exp_tab[i];
   const PairConst kc{a.eps, a.inveps, a.eps - 1.0, 1.0 - a.inveps};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
