@@ -17,7 +17,7 @@ import bipb_inputs as g  # noqa: E402
 import oracle  # noqa: E402
 
 
-def main(names, restarts=(20,)):
+def main(names, restarts=(20,), outdir=None):
     for name in names:
         p = g.config(name)
         out = {"config": name, "sha256": p.sha256(), "n": p.n, "nc": p.nc, "eps1": p.eps1, "eps2": p.eps2,
@@ -35,11 +35,12 @@ def main(names, restarts=(20,)):
                 "b_norm": float(np.linalg.norm(r["b"])), "x_norm": float(np.linalg.norm(r["x"]))}
             print(name, m, out["solves"][str(m)]["energy"], out["solves"][str(m)]["iterations"],
                   f"{time.time() - t:.1f}s", flush=True)
-        with open(os.path.join(ROOT, "tests", "golden", f"oracle_{name}.json"), "w") as f:
+        with open(os.path.join(outdir or os.path.join(ROOT, "tests", "golden"), f"oracle_{name}.json"), "w") as f:
             json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
-    args = sys.argv[1:] or ["C1", "C2"]
+    args = [a for a in sys.argv[1:] if not a.startswith("--out=")] or ["C1", "C2"]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
     ms = (10, 20) if all(a in ("C1", "C2") for a in args) else (20,)
-    main(args, ms)
+    main(args, ms, outs[0] if outs else None)

@@ -107,7 +107,7 @@ def test_solve_parity_small(bp, name, make, m, kind):
     ctx.close()
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
 def test_solve_parity_golden(bp, cfg):
     """Full-size BASELINE configs against stored oracle solves (tests/make_oracle_golden.py)."""
     path = os.path.join(GOLD, f"oracle_{cfg}.json")
