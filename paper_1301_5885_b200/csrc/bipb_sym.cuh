@@ -27,6 +27,10 @@ namespace bipb {
 #ifndef BIPB_SYM_PREFETCH
 #define BIPB_SYM_PREFETCH 1
 #endif
+// tuning variants of the per-step reverse accumulation (see the main loop); 0 = one chain
+#ifndef BIPB_SYM_RVSPLIT
+#define BIPB_SYM_RVSPLIT 0
+#endif
 
 // Record (tile-SoA): fields x, y, z (scaled by s), nx, ny, nz, then (c_r, a'_r) for r < R with
 // c = W u_dphi and a' = s W u_phi.  For every TILE-source tile the F = 6 + 2R fields are
@@ -256,6 +260,11 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
       Acc2 rv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) rv[r].p0 = rv[r].p1 = 0.0;
+#if BIPB_SYM_RVSPLIT == 1
+      Acc2 rv2[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) rv2[r].p0 = rv2[r].p1 = 0.0;
+#endif
       if (o != 0 && gcnt == 32) {
 #if BIPB_SYM_PREFETCH == 2
         // ping-pong record buffers: the next step's record loads while this step computes, with
@@ -296,6 +305,31 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
           SymSrc<R> sj;
           rec_load<R>(sb, g0 + ((lane + st) & 31), sj);
 #endif
+#if BIPB_SYM_RVSPLIT == 1
+          // two rotating accumulator sets (even / odd targets): halves the dependent FMA chain
+          // that ends each step, at the price of a second set of shuffles
+#pragma unroll
+          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], (k & 1) ? rv2 : rv);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
+            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
+            rv2[r].p0 = __shfl_sync(0xffffffffu, rv2[r].p0, (lane + 1) & 31);
+            rv2[r].p1 = __shfl_sync(0xffffffffu, rv2[r].p1, (lane + 1) & 31);
+          }
+#elif BIPB_SYM_RVSPLIT == 2
+          // odd targets into a fresh per-step accumulator, added once (one DADD per quantity)
+          Acc2 st2[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) st2[r].p0 = st2[r].p1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], (k & 1) ? st2 : rv);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0 + st2[r].p0, (lane + 1) & 31);
+            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1 + st2[r].p1, (lane + 1) & 31);
+          }
+#else
 #pragma unroll
           for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], rv);
 #pragma unroll
@@ -303,7 +337,15 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
             rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
             rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
           }
+#endif
         }
+#if BIPB_SYM_RVSPLIT == 1
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          rv[r].p0 += rv2[r].p0;
+          rv[r].p1 += rv2[r].p1;
+        }
+#endif
 #endif
       } else {
         // diagonal block (pairs i < j only) or a partial group

@@ -13,17 +13,17 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = []
-# symmetric-kernel launch shapes (TPB * T must be a multiple of the 128-source smem tile)
-for tpb, t, minb, pf, un, tile, stages in [(128, 5, 1, 1, 1, 128, 3), (128, 5, 1, 1, 1, 128, 2),
-                                           (128, 5, 1, 1, 1, 128, 4), (128, 5, 1, 1, 1, 64, 4),
-                                           (128, 4, 1, 1, 1, 256, 2), (128, 5, 1, 1, 1, 32, 6)]:
-    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 8, "pf": pf, "un": un,
-                     "tile": tile, "stages": stages})
+# symmetric-kernel variants: launch shape (TPB * T a multiple of the 128-source smem tile) plus
+# extra -D macros ("defs")
+for defs in ({}, {"BIPB_SYM_RVSPLIT": 1}, {"BIPB_SYM_RVSPLIT": 2}):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
+                     "tile": 128, "stages": 3, "defs": defs})
 
 
 def name(v):
+    extra = "".join(f"_{k.replace('BIPB_', '').lower()}{val}" for k, val in sorted(v.get("defs", {}).items()))
     return (f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}"
-            f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}")
+            f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}{extra}")
 
 
 def build():
@@ -39,6 +39,7 @@ def build():
                      f"-DBIPB_EXP_BITS={v['exp_bits']}", f"-DBIPB_SYM_PREFETCH={v.get('pf', 0)}",
                      f"-DBIPB_SYM_UNROLL={v.get('un', 1)}", f"-DBIPB_TILE={v.get('tile', 128)}",
                      f"-DBIPB_STAGES={v.get('stages', 3)}"]
+            extra += [f"-D{k}={val}" for k, val in v.get("defs", {}).items()]
         else:
             extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}"]
