@@ -164,6 +164,13 @@ def test_full_size_c4_sampled(bp):
     assert st == bp.OK and rep["rel_res_true"] <= 1e-9
     assert abs(e / ek - 1) < 5e-3
     assert 10 <= rep["iterations"] <= 60
+    # the GPU solution checked against the oracle's own equations (sampled rows of b - A x) and
+    # its full N_c x N energy sum (Eq. (14); 1.6e9 pairs, seconds on the host)
+    axi, axin = oracle.matvec_rows(p, x, rows)
+    bnorm = np.linalg.norm(b)
+    assert np.max(np.abs(bo[:rows.size] - axi)) <= 2e-9 * bnorm
+    assert np.max(np.abs(bo[rows.size:] - axin)) <= 2e-9 * bnorm
+    assert e == pytest.approx(oracle.energy(p, x), rel=1e-11)
     ctx.close()
 
 
