@@ -475,14 +475,22 @@ __global__ void reduce_sym_kernel(const double* __restrict__ fwd, const double* 
         }
       }
     }
-    for (int64_t o = 0; o <= hmax; ++o) {
-      const int64_t I = ((b - o) % nb + nb) % nb;
-      if (o >= sym_noff(I, nb) || I < Ia || I >= Ib) continue;
+    // offsets o whose source block I = b - o (mod nb) lies in [Ia, Ib): o = lo .. lo + L - 1
+    // (mod nb), visited in ascending o (two segments when the range wraps)
+    const int64_t L = Ib - Ia;
+    const int64_t lo = ((b - (Ib - 1)) % nb + nb) % nb;
+    const int64_t seg[2][2] = {{0, lo + L - 1 - nb}, {lo, lo + L - 1 < nb ? lo + L - 1 : nb - 1}};
+    for (int sgi = 0; sgi < 2; ++sgi) {
+      const int64_t oe = seg[sgi][1] < hmax ? seg[sgi][1] : hmax;
+      for (int64_t o = seg[sgi][0]; o <= oe; ++o) {
+        const int64_t I = ((b - o) % nb + nb) % nb;
+        if (o >= sym_noff(I, nb)) continue;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double* rv = rev + ((((I - Ia) * (hmax + 1) + o) * R + r) * 2) * B;
-        s0[r] += rv[l];
-        s1[r] += rv[B + l];
+        for (int r = 0; r < R; ++r) {
+          const double* rv = rev + ((((I - Ia) * (hmax + 1) + o) * R + r) * 2) * B;
+          s0[r] += rv[l];
+          s1[r] += rv[B + l];
+        }
       }
     }
 #pragma unroll
