@@ -28,9 +28,12 @@
  *
  * Multi-GPU (one process per GPU): pass a bipb_dist with the same 128-byte NCCL
  * unique id on every rank (create it with bipb_nccl_unique_id on rank 0 and
- * broadcast it).  Target rows are sharded (bipb_partition); every rank holds the full
- * geometry and charges, passes and receives full-length vectors, and runs the same
- * (replicated, deterministic) GMRES; an NCCL all-gather reassembles each product.
+ * broadcast it).  Every rank holds the full geometry and charges, passes and receives
+ * full-length vectors, and runs the same (replicated, deterministic) GMRES.  The product is
+ * sharded by kernel (bipb_set_matvec_kernel): the row kernel splits target rows
+ * (bipb_partition) and an NCCL all-gather reassembles y; the symmetric kernel splits its
+ * block schedule (bipb_partition of the 640-row blocks) and an NCCL all-reduce sums the
+ * ranks' partial row sums.  Source and energy shard target rows / charges + all-gather.
  */
 #ifndef BIPB_H
 #define BIPB_H
@@ -185,7 +188,7 @@ bipb_status bipb_nccl_unique_id(unsigned char* out);
  *   0  row kernel: every ordered pair (i, j) evaluated by the thread owning row i; a row's
  *      value is bitwise independent of the launch configuration and of the rank count.
  *   1  symmetric kernel: each unordered pair {i, j} evaluated once and used for both rows
- *      (K1, K4 symmetric; K2/K3 exchange under d -> -d); 28 instead of 48 FP64
+ *      (K1, K4 symmetric; K2/K3 exchange under d -> -d); 27.5 instead of 47 FP64
  *      instructions per ordered pair; deterministic for a fixed rank count; across ranks
  *      the partial products are summed with ncclAllReduce.
  * Default: 1 when the problem has at least one wave (296) of 640 x 640 tile pairs
