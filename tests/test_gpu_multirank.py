@@ -1,6 +1,6 @@
-"""The multi-rank code path on one GPU: 2 and 3 processes share the device and exchange through
-a test stand-in for NCCL (tests/fakenccl, selected with BIPB_NCCL_LIB; real NCCL refuses two
-ranks on one device).  Every rank runs the full pipeline (source -> replicated GMRES with one
+"""The multi-rank code path on one GPU: 2, 3 and 8 processes (8 = one 8-GPU box) share the device
+and exchange through a test stand-in for NCCL (tests/fakenccl, selected with BIPB_NCCL_LIB; real
+NCCL refuses two ranks on one device).  Every rank runs the full pipeline (source -> replicated GMRES with one
 collective per product -> energy) and must reproduce the single-GPU results: bitwise for the
 row kernel (rank-count invariant sums), to rounding for the symmetric kernel (all-reduce of
 partial sums)."""
@@ -63,7 +63,7 @@ def _spawn(world, kind):
 
 
 @pytest.mark.parametrize("kind", [0, 1])
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_multirank_matches_single(world, kind):
     assert os.path.exists(FAKE), "build tests/fakenccl/libfakenccl.so (__graft_entry__.build())"
     ref = _spawn(0, kind)[0]
