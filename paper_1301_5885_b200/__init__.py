@@ -84,10 +84,15 @@ def _check(st: int):
         raise BipbError(st, _lib.bipb_last_error().decode())
 
 
-def _ptr(a, writable=False):
-    """(pointer, keepalive) for a float64 C-contiguous numpy array or torch tensor."""
+def _ptr(a, writable=False, size=None):
+    """(pointer, keepalive) for a float64 C-contiguous numpy array or torch tensor holding
+    exactly `size` elements when given (the C ABI takes bare pointers)."""
     if a is None:
         return None, None
+    if size is not None:
+        have = a.size if isinstance(a, np.ndarray) else (a.numel() if hasattr(a, "numel") else None)
+        if have != size:
+            raise ValueError(f"array has {have} elements, expected {size}")
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or not a.flags.c_contiguous or (writable and not a.flags.writeable):
             raise ValueError("arrays must be float64, C-contiguous (and writable for outputs)")
@@ -171,10 +176,10 @@ def bipb_setup(centroids, normals, areas, charges, eps1, eps2, kappa, dist=None,
     cudaStream_t handle (int), e.g. torch.cuda.current_stream().cuda_stream."""
     n = int(centroids.shape[0])
     nc = int(charges.shape[0]) if charges is not None else 0
-    pc, kc = _ptr(centroids)
-    pn, kn = _ptr(normals)
-    pa, ka = _ptr(areas)
-    pq, kq = _ptr(charges) if nc > 0 else (None, None)
+    pc, kc = _ptr(centroids, size=3 * n)
+    pn, kn = _ptr(normals, size=3 * n)
+    pa, ka = _ptr(areas, size=n)
+    pq, kq = _ptr(charges, size=4 * nc) if nc > 0 else (None, None)
     d = None
     if dist is not None:
         rank, world, uid = dist[0], dist[1], dist[2]
@@ -199,7 +204,7 @@ def _out_like(ctx_n2, like):
 def bipb_source(ctx: Context, b=None):
     """Eq. (11): b = [S1; S2] (2n).  Returns b (a new numpy array if b is None)."""
     b = _out_like(2 * ctx.n, b)
-    pb, _ = _ptr(b, writable=True)
+    pb, _ = _ptr(b, writable=True, size=2 * ctx.n)
     _check(_lib.bipb_source(ctx.handle, pb))
     return b
 
@@ -207,8 +212,8 @@ def bipb_source(ctx: Context, b=None):
 def bipb_matvec(ctx: Context, u, y=None):
     """Eqs. (12)-(13): y = A u (2n)."""
     y = _out_like(2 * ctx.n, y)
-    pu, _ = _ptr(u)
-    py, _ = _ptr(y, writable=True)
+    pu, _ = _ptr(u, size=2 * ctx.n)
+    py, _ = _ptr(y, writable=True, size=2 * ctx.n)
     _check(_lib.bipb_matvec(ctx.handle, pu, py))
     return y
 
@@ -218,8 +223,8 @@ def bipb_matvec_batch(ctx: Context, U, Y=None):
     nrhs = int(U.shape[0])
     if Y is None:
         Y = np.empty((nrhs, 2 * ctx.n))
-    pu, _ = _ptr(U)
-    py, _ = _ptr(Y, writable=True)
+    pu, _ = _ptr(U, size=nrhs * 2 * ctx.n)
+    py, _ = _ptr(Y, writable=True, size=nrhs * 2 * ctx.n)
     _check(_lib.bipb_matvec_batch(ctx.handle, nrhs, pu, py))
     return Y
 
@@ -227,7 +232,7 @@ def bipb_matvec_batch(ctx: Context, U, Y=None):
 def bipb_set_charges(ctx: Context, charges):
     """Replace the point charges [nc, 4] (x, y, z, Q) on the same surface."""
     nc = int(charges.shape[0])
-    pq, _ = _ptr(charges) if nc > 0 else (None, None)
+    pq, _ = _ptr(charges, size=4 * nc) if nc > 0 else (None, None)
     _check(_lib.bipb_set_charges(ctx.handle, nc, pq))
     ctx.nc = nc
 
@@ -243,8 +248,8 @@ def bipb_gmres_solve_batch(ctx: Context, B, X, restart_m=20, tol=1e-10, max_iter
     for r in range(nrhs):
         reps[r].history = hist[r].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         reps[r].history_cap = cap
-    pb, _ = _ptr(B)
-    px, _ = _ptr(X, writable=True)
+    pb, _ = _ptr(B, size=nrhs * 2 * ctx.n)
+    px, _ = _ptr(X, writable=True, size=nrhs * 2 * ctx.n)
     st = _lib.bipb_gmres_solve_batch(ctx.handle, nrhs, pb, px, int(restart_m), float(tol), int(max_iters),
                                      int(check_true), reps)
     if st not in (OK, NOT_CONVERGED):
@@ -262,8 +267,8 @@ def bipb_gmres_solve(ctx: Context, x, b=None, restart_m=20, tol=1e-10, max_iters
                      history_cap=None, raise_on_not_converged=False):
     """GMRES(m) on the device.  x holds x0 on entry and the solution on
     return.  Returns (status, report dict)."""
-    px, _ = _ptr(x, writable=True)
-    pb, _ = _ptr(b)
+    px, _ = _ptr(x, writable=True, size=2 * ctx.n)
+    pb, _ = _ptr(b, size=2 * ctx.n)
     cap = max_iters + 1 if history_cap is None else history_cap
     hist = np.zeros(max(cap, 1))
     rep = Report(history=hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap=cap)
@@ -278,9 +283,9 @@ def bipb_gmres_solve(ctx: Context, x, b=None, restart_m=20, tol=1e-10, max_iters
 
 def bipb_energy(ctx: Context, x, phi_reac=None) -> float:
     """Eq. (14): E_sol [kcal/mol]; optionally fills phi_reac [nc]."""
-    px, _ = _ptr(x)
+    px, _ = _ptr(x, size=2 * ctx.n)
     e = np.zeros(1)
-    pp, _ = _ptr(phi_reac, writable=True) if phi_reac is not None else (None, None)
+    pp, _ = _ptr(phi_reac, writable=True, size=ctx.nc) if phi_reac is not None else (None, None)
     _check(_lib.bipb_energy(ctx.handle, px, e.ctypes.data, pp))
     return float(e[0])
 

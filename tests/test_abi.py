@@ -87,3 +87,26 @@ def test_header_documents_citations():
     txt = open(HDR).read()
     for cite in ("Eq. (11)", "Eqs. (12)-(13)", "Eq. (14)", "P:271-272", "eps2/eps1"):
         assert cite in txt
+
+
+def test_binding_rejects_wrong_sizes():
+    """The C ABI takes bare pointers: the binding checks every array's element count first."""
+    import paper_1301_5885_b200 as bp
+    ctx = bp.Context(ctypes.c_void_p(0), 4, 1, None)  # never reaches the library
+    with pytest.raises(ValueError):
+        bp.bipb_matvec(ctx, np.zeros(7))
+    with pytest.raises(ValueError):
+        bp.bipb_matvec(ctx, np.zeros(8), np.zeros(9))
+    with pytest.raises(ValueError):
+        bp.bipb_energy(ctx, np.zeros(8), np.zeros(2))
+    with pytest.raises(ValueError):
+        bp.bipb_gmres_solve(ctx, np.zeros(6))
+    with pytest.raises(ValueError):
+        bp.bipb_matvec_batch(ctx, np.zeros((2, 7)))
+    with pytest.raises(ValueError):
+        bp.bipb_setup(np.zeros((4, 3)), np.zeros((4, 3)), np.zeros(3), np.zeros((1, 4)), 1.0, 80.0, 0.1)
+    with pytest.raises(ValueError):
+        bp.bipb_setup(np.zeros((4, 3)), np.zeros((4, 3)), np.zeros(4), np.zeros((1, 3)), 1.0, 80.0, 0.1)
+    with pytest.raises(ValueError):
+        bp.bipb_matvec(ctx, np.zeros(8, dtype=np.float32))
+    ctx._h = None
