@@ -21,8 +21,8 @@
  *   Vectors of length 2N are laid out [phi_1..phi_N, dphi/dnu_1..dphi/dnu_N].
  *
  * Pointers: every array argument may be a HOST pointer or a DEVICE pointer on the
- * context's GPU (detected with cudaPointerGetAttributes).  Device pointers avoid
- * copies.  All calls are ordered on the context's CUDA stream and return after the
+ * context's GPU (detected with cudaPointerGetAttributes; a vector on another GPU is
+ * ERR_ARG).  Device pointers avoid copies.  All calls are ordered on the context's CUDA stream and return after the
  * work has completed.  A context is not thread-safe.  Errors are returned as status
  * codes, never as exceptions or aborts; bipb_last_error() gives a message.
  *

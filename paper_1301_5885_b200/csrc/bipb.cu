@@ -227,6 +227,11 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Where a vector argument lives: host memory (pageable or pinned) -> *dev = false; device or
+// managed memory of the context's GPU -> *dev = true; another GPU's memory -> ERR_ARG (the
+// kernels would read it through peer mappings that may not exist).
+static bipb_status vec_where(bipb_ctx* c, const void* p, bool* dev);
+
 static void launch_1d_cfg(int64_t work, int& grid, int& block) {
   block = 256;
   grid = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(work, block)), 148 * 8);
@@ -489,9 +494,26 @@ static bipb_status read_scalars(bipb_ctx* c, const double* dsrc, int count, doub
   return BIPB_OK;
 }
 
+static bipb_status vec_where(bipb_ctx* c, const void* p, bool* dev) {
+  *dev = false;
+  if (!p) return BIPB_OK;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return BIPB_OK;
+  }
+  if (at.type == cudaMemoryTypeDevice && at.device != c->device)
+    return fail(BIPB_ERR_ARG, "vector lives on GPU " + std::to_string(at.device) + ", the context on GPU " +
+                                  std::to_string(c->device));
+  *dev = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  return BIPB_OK;
+}
+
 // input vector -> device pointer (copying host data into `scratch`)
 static bipb_status in_vec(bipb_ctx* c, const double* p, int64_t len, double* scratch, const double** out) {
-  if (is_device_ptr(p)) {
+  bool dev;
+  CKS(vec_where(c, p, &dev));
+  if (dev) {
     *out = p;
     return BIPB_OK;
   }
@@ -809,7 +831,8 @@ bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
   const int64_t m2 = 2 * c->n;
   const double* ud;
   CKS(in_vec(c, u, m2, c->ubuf, &ud));
-  const bool ydev = is_device_ptr(y);
+  bool ydev;
+  CKS(vec_where(c, y, &ydev));
   double* yd = ydev ? y : c->ybuf;
   if (ydev && yd == ud) return fail(BIPB_ERR_ARG, "u and y must not alias");
   CKS(matvec_dev(c, ud, yd));
@@ -1128,7 +1151,8 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
   CKS(ensure_krylov(c, m));
   const double* bd = c->b;
   if (b) CKS(in_vec(c, b, m2, c->bbuf, &bd));
-  const bool xdev = is_device_ptr(x);
+  bool xdev;
+  CKS(vec_where(c, x, &xdev));
   double* xd = xdev ? x : c->xbuf;
   if (!xdev) CK(cudaMemcpyAsync(xd, x, m2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   double* S = c->scal;  // [0] ||b||, [1] beta, [2] hk1sq, [3] hk1, [4] ||x||^2
@@ -1219,7 +1243,9 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
   if (!c || !B || !X || nrhs < 1) return fail(BIPB_ERR_ARG, "NULL argument or nrhs < 1");
   if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
   const int64_t m2 = 2 * c->n;
-  const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
+  bool bdev, xdev;
+  CKS(vec_where(c, B, &bdev));
+  CKS(vec_where(c, X, &xdev));
   double *bst = nullptr, *xst = nullptr;
   if (!bdev) {
     CK(dmalloc(c, &bst, (size_t)nrhs * m2 * sizeof(double)));
@@ -1301,7 +1327,9 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
 bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double* Y) {
   if (!c || !U || !Y || nrhs < 1) return fail(BIPB_ERR_ARG, "bad argument");
   const int64_t m2 = 2 * c->n;
-  const bool udev = is_device_ptr(U), ydev = is_device_ptr(Y);
+  bool udev, ydev;
+  CKS(vec_where(c, U, &udev));
+  CKS(vec_where(c, Y, &ydev));
   // host operands are staged through device buffers in slices of up to 4 operands
   const int64_t slice = (udev && ydev) ? nrhs : 4;
   if (!(udev && ydev) && !c->bat_U) {
