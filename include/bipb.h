@@ -61,11 +61,21 @@ typedef enum {
 typedef struct {
   int32_t rank, world;       /* 0 <= rank < world */
   int32_t device;            /* CUDA device ordinal this rank uses (-1: current device) */
-  int32_t flags;             /* 0, or BIPB_DIST_NO_COMM (testing: no communicator; products
-                                and b contain only this rank's rows, the rest is zero) */
+  int32_t flags;             /* 0, BIPB_DIST_NO_COMM (testing: no communicator; products and b
+                                contain only this rank's rows, the rest is zero), or one of
+                                BIPB_DIST_P2P / BIPB_DIST_NCCL (exchange choice, see below) */
   unsigned char nccl_uid[128];
 } bipb_dist;
 #define BIPB_DIST_NO_COMM 1
+/* Per-product exchange (world > 1).  Default: peer stores — the product's epilogue kernel
+ * writes its rows / partial sums straight into every rank's mailbox (CUDA IPC mappings over
+ * NVLink / NVSwitch, set up once with NCCL all-gathers), then a flag handshake in device
+ * memory; used when every rank can map every other rank's memory (up to 16 ranks), else the
+ * NCCL collectives (all-gather / all-reduce).  Same values either way (row kernel: bitwise).
+ * BIPB_DIST_P2P forces peer stores (ERR_ARG if impossible, also at world 1), BIPB_DIST_NCCL
+ * forces the collectives; the environment variable BIPB_EXCHANGE=p2p|nccl overrides both. */
+#define BIPB_DIST_P2P 2
+#define BIPB_DIST_NCCL 4
 
 /* GMRES report (iterations, restarts, final residual, history). */
 typedef struct {

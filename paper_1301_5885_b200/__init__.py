@@ -37,6 +37,8 @@ class BipbError(RuntimeError):
 
 
 DIST_NO_COMM = 1
+DIST_P2P = 2  # force the peer-store exchange of the products (bipb.h; default when possible)
+DIST_NCCL = 4  # force NCCL collectives for the products
 
 
 class Dist(ctypes.Structure):

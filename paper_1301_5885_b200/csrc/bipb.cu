@@ -18,6 +18,7 @@
 #include "bipb_kernels.cuh"
 #include "bipb_vec.cuh"
 #include "bipb_sym.cuh"
+#include "bipb_p2p.cuh"
 
 using namespace bipb;
 
@@ -179,6 +180,16 @@ struct bipb_ctx {
   double* bat_U = nullptr;  // [4][2n] batch staging (host inputs)
   double* bat_Y = nullptr;
   int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
+  // peer-store exchange of the products (bipb_p2p.cuh; BIPB_DIST_P2P / BIPB_EXCHANGE=p2p)
+  bool p2p = false;
+  double* p2p_box = nullptr;                // own mailbox [2][stride] (cudaMalloc: IPC-exportable)
+  unsigned long long* p2p_flags = nullptr;  // own flags [world] (written by the peers)
+  unsigned long long* p2p_epoch = nullptr;  // own exchange counter (device)
+  int64_t p2p_stride = 0;
+  PeerBoxes boxes{};
+  PeerFlags flags{};
+  std::vector<void*> p2p_opened;  // peer mappings to close
+  unsigned long long p2p_timeout_ns = 120ull * 1000000000ull;
 
   bool timing = false;
   EventPool pool[3];
@@ -356,6 +367,16 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
   return BIPB_OK;
 }
 
+// ---- peer-store exchange (bipb_p2p.cuh): the producer kernel already stored its values into
+// every rank's mailbox; publish the epoch and wait for every rank's delivery.
+static bipb_status p2p_publish_and_wait(bipb_ctx* c) {
+  p2p_signal_kernel<<<1, 32, 0, c->stream>>>(c->p2p_epoch, c->flags, c->world, c->rank);
+  p2p_wait_kernel<<<1, 32, 0, c->stream>>>(c->p2p_epoch, c->p2p_flags, c->world, c->p2p_timeout_ns);
+  c->launches_all += 2;
+  CK(cudaGetLastError());
+  return BIPB_OK;
+}
+
 // ---- symmetric-pair products (bipb_sym.cuh) ------------------------------------------------
 static int sym_slot(int R) { return R == 1 ? 0 : (R == 2 ? 1 : 2); }
 
@@ -406,7 +427,15 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
   a.fwd = p->fwd; a.rev = p->rev;
   const size_t smem =
       sizeof(double) * (STAGES * TILE * SymLayout<R>::F + (Cfg::TPB / 32) * R * 2 * p->B) + 8 * STAGES;
-  if (p->I1 <= p->I0) CK(cudaMemsetAsync(c->sym_P, 0, (size_t)R * 2 * n * sizeof(double), c->stream));
+  const PeerBoxes nobox{};
+  if (p->I1 <= p->I0) {  // no I-blocks on this rank: its partial sums are zero
+    if (c->p2p) {
+      LAUNCH1D(reduce_sym_kernel<R>, n, p->fwd, p->rev, n, p->nb, p->B, p->runs, p->hmax, p->I0, p->I0, 1, c->sym_P,
+               c->boxes, c->world, c->rank, c->p2p_stride, c->p2p_epoch);
+    } else {
+      CK(cudaMemsetAsync(c->sym_P, 0, (size_t)R * 2 * n * sizeof(double), c->stream));
+    }
+  }
   for (int64_t Ia = p->I0; Ia < p->I1; Ia += p->group) {
     const int64_t Ib = std::min(Ia + p->group, p->I1);
     a.I0 = Ia;
@@ -425,8 +454,18 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
     }
     CK(cudaGetLastError());
     if (stop) CK(cudaEventRecord(stop, c->stream));
+    // the last group's epilogue stores the rank's row sums straight into every rank's mailbox
+    const bool to_peers = c->p2p && Ib == p->I1;
     LAUNCH1D(reduce_sym_kernel<R>, n, p->fwd, p->rev, n, p->nb, p->B, p->runs, p->hmax, Ia, Ib, Ia == p->I0 ? 1 : 0,
-             c->sym_P);
+             c->sym_P, to_peers ? c->boxes : nobox, to_peers ? c->world : 0, c->rank, c->p2p_stride,
+             c->p2p_epoch);
+  }
+  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
+  if (c->p2p) {
+    CKS(p2p_publish_and_wait(c));
+    LAUNCH1D(finish_sym_p2p_kernel<R>, n, c->p2p_box, c->p2p_stride, c->p2p_epoch, c->world, U, n, d1, d2, Y);
+    c->matvec_calls += R;
+    return BIPB_OK;
   }
   if (c->sharded && !c->no_comm) {  // every rank holds partial sums for all rows
     NcclApi& api = nccl();
@@ -434,7 +473,6 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
         api.AllReduce(c->sym_P, c->sym_P, (size_t)(R * 2 * n), ncclFloat64, ncclSum, c->comm, c->stream);
     if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
   }
-  const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
   LAUNCH1D(finish_sym_kernel<R>, n, c->sym_P, U, n, d1, d2, Y);
   c->matvec_calls += R;
   return BIPB_OK;
@@ -471,6 +509,11 @@ static bipb_status matvec_dev_impl(bipb_ctx* c, const double* u, double* y) {
   const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
   if (!c->sharded) {
     LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u, u + n, d1, d2, y, y + n);
+  } else if (c->p2p) {  // epilogue stores the rank's rows into every rank's mailbox
+    LAUNCH1D(reduce_matvec_p2p_kernel, std::max<int64_t>(nloc, 1), c->part, c->nchunk_mv, nloc, u + c->r0,
+             u + n + c->r0, d1, d2, c->r0, n, c->boxes, c->world, c->p2p_stride, c->p2p_epoch);
+    CKS(p2p_publish_and_wait(c));
+    LAUNCH1D(p2p_take_kernel, 2 * n, c->p2p_box, c->p2p_stride, c->p2p_epoch, 2 * n, y);
   } else {
     LAUNCH1D(reduce_matvec_kernel, nloc, c->part, c->nchunk_mv, nloc, u + c->r0, u + n + c->r0, d1, d2, c->stage,
              c->stage + c->np);
@@ -566,6 +609,11 @@ void bipb_destroy(bipb_ctx* c) {
   }
   if (c->red_cnt) dfree(c, c->red_cnt);
   if (c->dflag) dfree(c, c->dflag);
+  if (c->p2p_epoch) dfree(c, c->p2p_epoch);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
+  if (c->p2p_box) cudaFree(c->p2p_box);
+  if (c->p2p_flags) cudaFree(c->p2p_flags);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (auto& p : c->pool)
     for (auto e : p.ev) cudaEventDestroy(e);
@@ -627,6 +675,87 @@ static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<doubl
     CK(cudaStreamSynchronize(c->stream));
     if (flag) return fail(BIPB_ERR_SINGULAR, "a charge lies within 1e-6 A of an element centroid");
   }
+  return BIPB_OK;
+}
+
+// Peer-store exchange (bipb_p2p.cuh): mailbox + flags in cudaMalloc memory (IPC-exportable),
+// handles all-gathered once over the communicator and opened on every rank.  `require`: fail
+// unless every rank can map every other rank's memory; otherwise (auto) a rank pair without
+// peer access makes ALL ranks keep the NCCL collectives (the decision is all-gathered).
+static bipb_status p2p_setup(bipb_ctx* c, bool require) {
+  if (c->world > P2P_MAX) return fail(BIPB_ERR_ARG, "the peer-store exchange supports up to 16 ranks");
+  if (const char* e = getenv("BIPB_P2P_TIMEOUT_S")) c->p2p_timeout_ns = (unsigned long long)(atof(e) * 1e9);
+  const int64_t m2 = 2 * c->n;
+  c->p2p_stride = (int64_t)c->world * 4 * m2;  // symmetric slots [world][R <= 4][2n]; row kernel [2n]
+  CK(cudaMalloc(&c->p2p_box, 2 * (size_t)c->p2p_stride * sizeof(double)));
+  CK(cudaMalloc(&c->p2p_flags, (size_t)c->world * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(c->p2p_flags, 0, (size_t)c->world * sizeof(unsigned long long), c->stream));
+  CK(dmalloc(c, &c->p2p_epoch, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(c->p2p_epoch, 0, sizeof(unsigned long long), c->stream));
+  c->boxes.p[c->rank] = c->p2p_box;
+  c->flags.p[c->rank] = c->p2p_flags;
+  if (c->world > 1) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    constexpr int W = 17;  // per rank: box handle (8 doubles), flags handle (8), device ordinal
+    cudaIpcMemHandle_t hb, hf;
+    CK(cudaIpcGetMemHandle(&hb, c->p2p_box));
+    CK(cudaIpcGetMemHandle(&hf, c->p2p_flags));
+    double mine[W];
+    memcpy(mine, &hb, 64);
+    memcpy(mine + 8, &hf, 64);
+    mine[16] = (double)c->device;
+    double *dsend = nullptr, *drecv = nullptr;
+    CK(dmalloc(c, &dsend, W * sizeof(double)));
+    CK(dmalloc(c, &drecv, (size_t)c->world * W * sizeof(double)));
+    std::vector<double> all((size_t)c->world * W);
+    NcclApi& api = nccl();
+    auto allgather = [&](const double* src, int cnt, double* dst) -> bipb_status {
+      CK(cudaMemcpyAsync(dsend, src, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      ncclResult_t r = api.AllGather(dsend, drecv, (size_t)cnt, ncclFloat64, c->comm, c->stream);
+      if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather (p2p setup): ") + api.GetErrorString(r));
+      CK(cudaMemcpyAsync(dst, drecv, (size_t)c->world * cnt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      return BIPB_OK;
+    };
+    CKS(allgather(mine, W, all.data()));
+    // can this rank map every peer's memory?  (same device: IPC within the GPU)
+    double ok = 1.0;
+    for (int q = 0; q < c->world; ++q) {
+      const int dq = (int)all[(size_t)q * W + 16];
+      int can = 1;
+      if (dq != c->device && cudaDeviceCanAccessPeer(&can, c->device, dq) != cudaSuccess) can = 0;
+      if (!can) ok = 0.0;
+    }
+    std::vector<double> oks((size_t)c->world);
+    CKS(allgather(&ok, 1, oks.data()));
+    dfree(c, dsend);
+    dfree(c, drecv);
+    bool all_ok = true;
+    for (double v : oks) all_ok = all_ok && v != 0.0;
+    if (!all_ok) {
+      cudaGetLastError();
+      if (require) return fail(BIPB_ERR_ARG, "BIPB_DIST_P2P: some rank cannot access a peer's memory");
+      CK(cudaFree(c->p2p_box));
+      CK(cudaFree(c->p2p_flags));
+      c->p2p_box = nullptr;
+      c->p2p_flags = nullptr;
+      return BIPB_OK;  // NCCL collectives (c->p2p stays false)
+    }
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      memcpy(&hb, &all[(size_t)q * W], 64);
+      memcpy(&hf, &all[(size_t)q * W + 8], 64);
+      void *pb = nullptr, *pf = nullptr;
+      CK(cudaIpcOpenMemHandle(&pb, hb, cudaIpcMemLazyEnablePeerAccess));
+      c->p2p_opened.push_back(pb);
+      CK(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
+      c->p2p_opened.push_back(pf);
+      c->boxes.p[q] = static_cast<double*>(pb);
+      c->flags.p[q] = static_cast<unsigned long long*>(pf);
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->p2p = true;
   return BIPB_OK;
 }
 
@@ -760,6 +889,15 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     memcpy(&id, dist->nccl_uid, 128);
     ncclResult_t r = api.CommInitRank(&c->comm, c->world, id, c->rank);
     if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+    // per-product exchange: peer stores (default when world > 1 and every rank can map every
+    // peer) or NCCL collectives; flags BIPB_DIST_P2P / BIPB_DIST_NCCL and BIPB_EXCHANGE=p2p|nccl
+    // force one
+    int mode = (dist->flags & BIPB_DIST_P2P) ? 1 : ((dist->flags & BIPB_DIST_NCCL) ? 0 : 2);  // 2 = auto
+    if (const char* e = getenv("BIPB_EXCHANGE")) {
+      if (!strcmp(e, "p2p")) mode = 1;
+      if (!strcmp(e, "nccl")) mode = 0;
+    }
+    if (mode == 1 || (mode == 2 && c->world > 1)) CKS(p2p_setup(c, mode == 1));
   }
   CK(cudaStreamSynchronize(c->stream));
   tr.mark("nccl + sync");

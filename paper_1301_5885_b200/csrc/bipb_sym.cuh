@@ -21,6 +21,7 @@
 // I-blocks in groups (bounded partial memory); groups are summed in order.
 #pragma once
 #include "bipb_kernels.cuh"
+#include "bipb_p2p.cuh"
 
 namespace bipb {
 
@@ -453,10 +454,14 @@ __global__ void prescale_sym_kernel(const double* __restrict__ U, const double* 
 // For global row i (block b, local l): forward runs of block b (if b is in [Ia, Ib)) in run
 // order, then reverse offsets o = 0..hmax of the tiles (I = b - o mod nb, J = b) with I in
 // [Ia, Ib) and o < noff(I).  Fixed order -> deterministic.
+// With nbox > 0 (last group, peer-store exchange) the row sums go to slot [rank] of every rank's
+// mailbox (bipb_p2p.cuh) instead of P.
 template <int R>
 __global__ void reduce_sym_kernel(const double* __restrict__ fwd, const double* __restrict__ rev, int64_t n,
                                   int64_t nb, int64_t B, int64_t runs, int64_t hmax, int64_t Ia, int64_t Ib,
-                                  int first, double* __restrict__ P) {
+                                  int first, double* __restrict__ P, const PeerBoxes box, int nbox, int rank,
+                                  int64_t stride, const unsigned long long* __restrict__ epoch) {
+  const int64_t boff = nbox > 0 ? p2p_next_parity(epoch) * stride + (int64_t)rank * R * 2 * n : 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = i / B, l = i % B;
     double s0[R], s1[R];
@@ -493,10 +498,21 @@ __global__ void reduce_sym_kernel(const double* __restrict__ fwd, const double* 
         }
       }
     }
+    if (nbox > 0) {
+      for (int p = 0; p < nbox; ++p) {
+        double* b = box.p[p] + boff;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      P[(int64_t)(2 * r) * n + i] = s0[r];
-      P[(int64_t)(2 * r + 1) * n + i] = s1[r];
+        for (int r = 0; r < R; ++r) {
+          b[(int64_t)(2 * r) * n + i] = s0[r];
+          b[(int64_t)(2 * r + 1) * n + i] = s1[r];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        P[(int64_t)(2 * r) * n + i] = s0[r];
+        P[(int64_t)(2 * r + 1) * n + i] = s1[r];
+      }
     }
   }
 }

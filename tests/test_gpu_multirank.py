@@ -1,6 +1,7 @@
 """The multi-rank code path on one GPU: 2, 3 and 8 processes (8 = one 8-GPU box) share the device
 and exchange through a test stand-in for NCCL (tests/fakenccl, selected with BIPB_NCCL_LIB; real
-NCCL refuses two ranks on one device).  Every rank runs the full pipeline (source -> replicated GMRES with one
+NCCL refuses two ranks on one device), or through the peer-store exchange (CUDA IPC mailboxes,
+bipb_p2p.cuh).  Every rank runs the full pipeline (source -> replicated GMRES with one
 collective per product -> energy) and must reproduce the single-GPU results: bitwise for the
 row kernel (rank-count invariant sums), to rounding for the symmetric kernel (all-reduce of
 partial sums)."""
@@ -20,9 +21,10 @@ def _problem():
     return g.sphere_problem(5, 4.0, g.charges_in_ball(30, 3.0, 17))  # N = 20480 (symmetric default)
 
 
-def _run(rank, world, uid, kind, q):
+def _run(rank, world, uid, kind, exchange, q):
     os.environ["BIPB_NCCL_LIB"] = FAKE
     os.environ["BIPB_GRAPHS"] = "0"  # the stand-in synchronises inside collectives: not capturable
+    os.environ["BIPB_EXCHANGE"] = exchange  # nccl: collectives; p2p: peer stores (bipb_p2p.cuh)
     try:
         import paper_1301_5885_b200 as bp
         p = _problem()
@@ -43,7 +45,7 @@ def _run(rank, world, uid, kind, q):
         q.put((rank, None, repr(ex)))
 
 
-def _spawn(world, kind):
+def _spawn(world, kind, exchange="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     uid = None
@@ -51,7 +53,7 @@ def _spawn(world, kind):
         # must not load the stand-in into its own copy of the library)
         import time
         uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
-    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, q)) for r in range(max(world, 1))]
+    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, exchange, q)) for r in range(max(world, 1))]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -62,12 +64,13 @@ def _spawn(world, kind):
     return [r[1] for r in sorted(res, key=lambda t: t[0])]
 
 
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
 @pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_multirank_matches_single(world, kind):
+def test_multirank_matches_single(world, kind, exchange):
     assert os.path.exists(FAKE), "build tests/fakenccl/libfakenccl.so (__graft_entry__.build())"
     ref = _spawn(0, kind)[0]
-    outs = _spawn(world, kind)
+    outs = _spawn(world, kind, exchange)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
     for o in outs:  # every rank holds the full, identical result
         assert np.array_equal(o["x"], outs[0]["x"]) and o["e"] == outs[0]["e"]

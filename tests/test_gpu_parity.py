@@ -281,11 +281,13 @@ def test_row_shards_bitwise_equal_single_gpu(bp, world):
     assert e1 == pytest.approx(0.5 * 4 * np.pi * 332.0716 * float(np.dot(p.charges[:, 3], phi)), rel=1e-13)
 
 
+@pytest.mark.parametrize("flags", [0, 2])
 @pytest.mark.parametrize("kind", [0, 1])
-def test_nccl_exchange_path_world1(bp, kind):
+def test_nccl_exchange_path_world1(bp, kind, flags):
     """The real NCCL exchange path (dlopen'ed libnccl, unique id, communicator, all-gather
     (row kernel) / all-reduce (symmetric kernel) on the library stream) on a world-1
-    communicator equals the unsharded path bitwise."""
+    communicator equals the unsharded path bitwise; flags = DIST_P2P: the peer-store exchange
+    (mailbox, epoch flags, fused epilogue stores) instead of the collective."""
     import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library reuses)
     p = g.sphere_problem(3, 4.0, g.charges_in_ball(23, 3.0, 6))
     ref = _ctx(bp, p)
@@ -298,7 +300,8 @@ def test_nccl_exchange_path_world1(bp, kind):
     ref.close()
     uid = bp.bipb_nccl_unique_id()
     assert len(uid) == 128
-    c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=(0, 1, uid, 0))
+    c = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa,
+                      dist=(0, 1, uid, 0, flags))
     c.set_matvec_kernel(kind)
     y = bp.bipb_matvec(c, u)
     if kind == 0:
