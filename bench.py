@@ -59,7 +59,7 @@ def parse():
 def bench_config(prob, world):
     return {"workload": prob.name, "n_elements": prob.n, "n_charges": prob.nc, "restart_m": RESTART_M, "tol": TOL,
             "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
-            "parallelism": f"shard x{world} + one NCCL collective per matvec",
+            "parallelism": f"shard x{world}, one exchange of the product per matvec" if world > 1 else "single GPU",
             "l2": "flushed between steps (256 MiB)"}
 
 
@@ -283,7 +283,7 @@ def run_native(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges, bipb_inputs)",
-            "config": bench_config(prob, world),
+            "config": dict(bench_config(prob, world), exchange=ctx.exchange),
             "time_to_solution_s": total_ms / args.steps / 1e3,
             "iterations": [r["iterations"] for r in reps], "matvecs": matvecs,
             "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),

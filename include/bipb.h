@@ -207,6 +207,10 @@ bipb_status bipb_nccl_unique_id(unsigned char* out);
 bipb_status bipb_set_matvec_kernel(bipb_ctx* ctx, int32_t kind);
 int32_t bipb_get_matvec_kernel(bipb_ctx* ctx);
 
+/* How products are exchanged between ranks: 0 none (one GPU or BIPB_DIST_NO_COMM),
+ * 1 NCCL collectives, 2 peer stores (BIPB_DIST_P2P above); -1 for a NULL context. */
+int32_t bipb_get_exchange(bipb_ctx* ctx);
+
 /*
  * Instrumentation (bench.py, tests).  `which`: 0 = matvec pair kernel, 1 = source pair
  * kernel, 2 = energy pair kernel, 3 = all kernels of the library.

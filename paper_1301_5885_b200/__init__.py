@@ -74,6 +74,7 @@ _SIGS = {
     "bipb_gmres_solve_batch": ([_P, _I32, _P, _P, _I32, _D, _I32, _I32, ctypes.POINTER(Report)], ctypes.c_int),
     "bipb_set_charges": ([_P, _I64, _P], ctypes.c_int),
     "bipb_get_matvec_kernel": ([_P], _I32),
+    "bipb_get_exchange": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_a, _r) in _SIGS.items():
@@ -158,6 +159,11 @@ class Context:
     @property
     def matvec_kernel(self) -> int:
         return int(_lib.bipb_get_matvec_kernel(self.handle))
+
+    @property
+    def exchange(self) -> str:
+        """How products are exchanged between ranks: "none", "nccl" or "p2p" (peer stores)."""
+        return {0: "none", 1: "nccl", 2: "p2p"}[int(_lib.bipb_get_exchange(self.handle))]
 
     # instrumentation (bench.py) -------------------------------------------------
     def timing_enable(self, on=True):
@@ -299,6 +305,11 @@ def bipb_set_matvec_kernel(ctx: Context, kind: int):
 
 def bipb_get_matvec_kernel(ctx: Context) -> int:
     return ctx.matvec_kernel
+
+
+def bipb_get_exchange(ctx: Context) -> int:
+    """0 none, 1 NCCL collectives, 2 peer stores (bipb.h)."""
+    return int(_lib.bipb_get_exchange(ctx.handle))
 
 
 def bipb_destroy(ctx: Context):

@@ -1516,6 +1516,12 @@ bipb_status bipb_set_matvec_kernel(bipb_ctx* c, int32_t kind) {
 
 int32_t bipb_get_matvec_kernel(bipb_ctx* c) { return c ? c->mv_kind : -1; }
 
+int32_t bipb_get_exchange(bipb_ctx* c) {
+  if (!c) return -1;
+  if (!c->sharded || c->no_comm) return 0;
+  return c->p2p ? 2 : 1;
+}
+
 bipb_status bipb_timing_enable(bipb_ctx* c, int32_t on) {
   if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
   c->timing = on != 0;

@@ -54,3 +54,4 @@ def test_native_arm_two_ranks_one_gpu():
     assert len(lines) == 1  # rank 0 only
     d = json.loads(lines[0])
     assert REQUIRED <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "strong" and "cpu_baseline" not in d
+    assert d["config"]["exchange"] == "p2p"  # default: peer stores (both ranks map each other's mailbox)

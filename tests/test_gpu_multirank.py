@@ -31,6 +31,7 @@ def _run(rank, world, uid, kind, exchange, q):
         dist = None if world == 0 else (rank, world, uid, 0)
         ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
         ctx.set_matvec_kernel(kind)
+        assert ctx.exchange == ("none" if world == 0 else exchange)
         u = g.random_vector(2 * p.n, 5)
         y = bp.bipb_matvec(ctx, u)
         Y = bp.bipb_matvec_batch(ctx, np.stack([u, 2 * u, -u]))
