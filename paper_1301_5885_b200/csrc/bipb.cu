@@ -950,6 +950,11 @@ bipb_status bipb_source(bipb_ctx* c, double* b) {
     const double scale = 1.0 / (FOUR_PI * c->eps1);
     if (!c->sharded) {
       LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->b, c->b + n);
+    } else if (c->p2p) {
+      LAUNCH1D(reduce_source_p2p_kernel, std::max<int64_t>(nloc, 1), c->part, c->nchunk_src, nloc, scale, c->r0, n,
+               c->boxes, c->world, c->p2p_stride, c->p2p_epoch);
+      CKS(p2p_publish_and_wait(c));
+      LAUNCH1D(p2p_take_kernel, 2 * n, c->p2p_box, c->p2p_stride, c->p2p_epoch, 2 * n, c->b);
     } else {
       LAUNCH1D(reduce_source_kernel, nloc, c->part, c->nchunk_src, nloc, scale, c->stage, c->stage + c->np);
       CKS(allgather_rows(c, c->b));
@@ -1432,6 +1437,11 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
     CKS((launch_pair<ENERGY, EN_TPB, EN_T, EN_MINB>(c, a, c->nchunk_en, 2)));
     if (!c->sharded) {
       LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->phit);
+    } else if (c->p2p && nc <= c->p2p_stride) {
+      LAUNCH1D(reduce_energy_p2p_kernel, std::max<int64_t>(kloc, 1), c->part, c->nchunk_en, kloc, c->k0, c->boxes,
+               c->world, c->p2p_stride, c->p2p_epoch);
+      CKS(p2p_publish_and_wait(c));
+      LAUNCH1D(p2p_take_kernel, nc, c->p2p_box, c->p2p_stride, c->p2p_epoch, nc, c->phit);
     } else {
       LAUNCH1D(reduce_energy_kernel, kloc, c->part, c->nchunk_en, kloc, c->stage);
       if (c->no_comm) {

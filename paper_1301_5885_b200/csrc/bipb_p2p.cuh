@@ -6,7 +6,8 @@
 // setup: box[2 parities][stride] doubles plus a flag word per rank.  One exchange =
 //   1. the product's epilogue kernel computes its values and STORES them straight into every
 //      rank's mailbox (row kernel: rows [r0, r1) at their global positions; symmetric kernel:
-//      this rank's partial sums of all rows into slot [rank]);
+//      this rank's partial sums of all rows into slot [rank]; likewise the source term's rows
+//      and the energy's per-charge potentials);
 //   2. p2p_signal_kernel: system-scope fence, epoch += 1, release-store the epoch into flag
 //      [rank] of every rank;
 //   3. p2p_wait_kernel: acquire-spin until every rank's flag in the OWN flag array reached the
@@ -66,6 +67,39 @@ __global__ void reduce_matvec_p2p_kernel(const double* __restrict__ part, int64_
       b[r0 + l] = v0;
       b[n + r0 + l] = v1;
     }
+  }
+}
+
+// Source term epilogue + exchange (same arithmetic as reduce_source_kernel): b rows r0 + l and
+// n + r0 + l of every rank's mailbox.
+__global__ void reduce_source_p2p_kernel(const double* __restrict__ part, int64_t nchunk, int64_t ntgt, double scale,
+                                         int64_t r0, int64_t n, const PeerBoxes box, int world, int64_t stride,
+                                         const unsigned long long* __restrict__ epoch) {
+  const int64_t off = static_cast<int64_t>(p2p_next_parity(epoch)) * stride;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t c = 0; c < nchunk; ++c) {
+      s0 += part[(2 * c) * ntgt + l];
+      s1 += part[(2 * c + 1) * ntgt + l];
+    }
+    for (int p = 0; p < world; ++p) {
+      double* b = box.p[p] + off;
+      b[r0 + l] = s0 * scale;
+      b[n + r0 + l] = s1 * scale;
+    }
+  }
+}
+
+// Energy epilogue + exchange (same arithmetic as reduce_energy_kernel): phi_tilde of charges
+// k0 + l into every rank's mailbox.
+__global__ void reduce_energy_p2p_kernel(const double* __restrict__ part, int64_t nchunk, int64_t ntgt, int64_t k0,
+                                         const PeerBoxes box, int world, int64_t stride,
+                                         const unsigned long long* __restrict__ epoch) {
+  const int64_t off = static_cast<int64_t>(p2p_next_parity(epoch)) * stride;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
+    double s0 = 0.0;
+    for (int64_t c = 0; c < nchunk; ++c) s0 += part[(2 * c) * ntgt + l];
+    for (int p = 0; p < world; ++p) box.p[p][off + k0 + l] = s0;
   }
 }
 
