@@ -17,17 +17,19 @@ pytestmark = pytest.mark.gpu
 FAKE = os.path.join(os.path.dirname(__file__), "fakenccl", "libfakenccl.so")
 
 
-def _problem():
+def _problem(size="big"):
+    if size == "tiny":  # 20 elements, 3 charges: most ranks own no rows, blocks or charges
+        return g.sphere_problem(0, 4.0, g.charges_in_ball(3, 2.0, 5))
     return g.sphere_problem(5, 4.0, g.charges_in_ball(30, 3.0, 17))  # N = 20480 (symmetric default)
 
 
-def _run(rank, world, uid, kind, exchange, q):
+def _run(rank, world, uid, kind, exchange, q, size="big"):
     os.environ["BIPB_NCCL_LIB"] = FAKE
     os.environ["BIPB_GRAPHS"] = "0"  # the stand-in synchronises inside collectives: not capturable
     os.environ["BIPB_EXCHANGE"] = exchange  # nccl: collectives; p2p: peer stores (bipb_p2p.cuh)
     try:
         import paper_1301_5885_b200 as bp
-        p = _problem()
+        p = _problem(size)
         dist = None if world == 0 else (rank, world, uid, 0)
         ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
         ctx.set_matvec_kernel(kind)
@@ -46,7 +48,7 @@ def _run(rank, world, uid, kind, exchange, q):
         q.put((rank, None, repr(ex)))
 
 
-def _spawn(world, kind, exchange="nccl"):
+def _spawn(world, kind, exchange="nccl", size="big"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     uid = None
@@ -54,7 +56,7 @@ def _spawn(world, kind, exchange="nccl"):
         # must not load the stand-in into its own copy of the library)
         import time
         uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
-    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, exchange, q)) for r in range(max(world, 1))]
+    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, exchange, q, size)) for r in range(max(world, 1))]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -84,3 +86,18 @@ def test_multirank_matches_single(world, kind, exchange):
             assert np.array_equal(o["b"], ref["b"])
             assert rel(o["x"], ref["x"]) <= 1e-11 and o["e"] == pytest.approx(ref["e"], rel=1e-12)
         np.testing.assert_allclose(o["phi"], ref["phi"], rtol=1e-13, atol=1e-16)
+
+
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_multirank_tiny_problem(kind, exchange):
+    """8 ranks on a 20-element surface with 3 charges: ranks without rows, I-blocks or charges
+    still take part in every exchange (zero contributions) and end with the single-GPU result."""
+    ref = _spawn(0, kind, size="tiny")[0]
+    outs = _spawn(8, kind, exchange, size="tiny")
+    for o in outs:
+        assert o["its"] == ref["its"]
+        np.testing.assert_allclose(o["y"], ref["y"], rtol=1e-14, atol=1e-15 * np.abs(ref["y"]).max())
+        np.testing.assert_allclose(o["x"], ref["x"], rtol=1e-11, atol=1e-13 * np.abs(ref["x"]).max())
+        assert np.array_equal(o["b"], ref["b"])
+        assert o["e"] == pytest.approx(ref["e"], rel=1e-12)
