@@ -15,7 +15,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 VARIANTS = []
 # symmetric-kernel variants: launch shape (TPB * T a multiple of the 128-source smem tile) plus
 # extra -D macros ("defs")
-for defs in ({}, {"BIPB_RSQ_NEWTON": 1}):
+for defs in ({}, {"BIPB_RSQ_INT": 1}, {"BIPB_EXP_F32K": 1}, {"BIPB_RSQ_INT": 1, "BIPB_EXP_F32K": 1}):
     VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
                      "tile": 128, "stages": 3, "defs": defs})
 
