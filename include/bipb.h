@@ -211,6 +211,16 @@ int32_t bipb_get_matvec_kernel(bipb_ctx* ctx);
  * 1 NCCL collectives, 2 peer stores (BIPB_DIST_P2P above); -1 for a NULL context. */
 int32_t bipb_get_exchange(bipb_ctx* ctx);
 
+/* How bipb_gmres_solve runs the orthogonalisation of each Arnoldi step (same algorithm: modified
+ * Gram-Schmidt, Givens rotation, normalisation):
+ *   0   one reduction kernel per MGS dot product (k + 4 launches in step k)
+ *   E>0 one kernel on one 8-CTA thread-block cluster, E vector elements per thread in registers,
+ *       the dot products reduced through distributed shared memory (2N <= 8 * 1024 * E; chosen
+ *       at setup for 2N <= 65536, i.e. N <= 32768; BIPB_ARNOLDI=launches in the environment
+ *       forces 0).  Deterministic; only the summation order of the dots differs from 0.
+ * -1 for a NULL context. */
+int32_t bipb_get_arnoldi(bipb_ctx* ctx);
+
 /*
  * Instrumentation (bench.py, tests).  `which`: 0 = matvec pair kernel, 1 = source pair
  * kernel, 2 = energy pair kernel, 3 = all kernels of the library.

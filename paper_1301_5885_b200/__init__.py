@@ -75,6 +75,7 @@ _SIGS = {
     "bipb_set_charges": ([_P, _I64, _P], ctypes.c_int),
     "bipb_get_matvec_kernel": ([_P], _I32),
     "bipb_get_exchange": ([_P], _I32),
+    "bipb_get_arnoldi": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_a, _r) in _SIGS.items():
@@ -164,6 +165,11 @@ class Context:
     def exchange(self) -> str:
         """How products are exchanged between ranks: "none", "nccl" or "p2p" (peer stores)."""
         return {0: "none", 1: "nccl", 2: "p2p"}[int(_lib.bipb_get_exchange(self.handle))]
+
+    @property
+    def arnoldi(self) -> int:
+        """0: one launch per MGS reduction; E > 0: fused cluster kernel, E elements per thread."""
+        return int(_lib.bipb_get_arnoldi(self.handle))
 
     # instrumentation (bench.py) -------------------------------------------------
     def timing_enable(self, on=True):
@@ -310,6 +316,11 @@ def bipb_get_matvec_kernel(ctx: Context) -> int:
 def bipb_get_exchange(ctx: Context) -> int:
     """0 none, 1 NCCL collectives, 2 peer stores (bipb.h)."""
     return int(_lib.bipb_get_exchange(ctx.handle))
+
+
+def bipb_get_arnoldi(ctx: Context) -> int:
+    """0 multi-launch MGS, E > 0 fused cluster Arnoldi kernel (bipb.h)."""
+    return int(_lib.bipb_get_arnoldi(ctx.handle))
 
 
 def bipb_destroy(ctx: Context):

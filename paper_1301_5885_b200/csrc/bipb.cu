@@ -167,6 +167,8 @@ struct bipb_ctx {
   double* red_part = nullptr;
   unsigned* red_cnt = nullptr;
   double* host_info = nullptr;  // pinned [4]
+  double* host_info_dev = nullptr;  // its device mapping (UVA), or null
+  int arn_E = -1;                   // fused Arnoldi tail: elements per thread (0 = multi-launch MGS)
   int* dflag = nullptr;
 
   // symmetric matvec (bipb_sym.cuh): one schedule per R in {1, 2, 4}
@@ -855,6 +857,23 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   CK(cudaMemsetAsync(c->red_cnt, 0, sizeof(unsigned), c->stream));
   CK(dmalloc(c, &c->dflag, sizeof(int)));
   CK(cudaMallocHost(&c->host_info, 8 * sizeof(double)));
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, c->host_info) == cudaSuccess && pa.devicePointer)
+      c->host_info_dev = static_cast<double*>(pa.devicePointer);
+    cudaGetLastError();
+  }
+  {  // fused Arnoldi tail when the Krylov vectors fit one cluster's registers (BIPB_ARNOLDI=launches: off)
+    const char* ae = getenv("BIPB_ARNOLDI");
+    const bool force_off = ae && !strcmp(ae, "launches");
+    c->arn_E = 0;
+    if (!force_off)
+      for (int E : {1, 2, 4, 8})
+        if ((int64_t)ARN_CLUSTER * ARN_THREADS * E >= m2) {
+          c->arn_E = E;
+          break;
+        }
+  }
 
   tr.mark("upload + buffers");
   // ---- launch geometry (global sizes only => P-invariant sums)
@@ -1038,6 +1057,19 @@ static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
   double* vk = c->V + (int64_t)k * m2;
   double* w = c->V + (int64_t)(k + 1) * m2;
   CKS(matvec_dev(c, vk, w));
+  if (c->arn_E > 0) {  // MGS + Givens + normalisation in one cluster kernel (bipb_vec.cuh)
+    switch (c->arn_E) {
+      case 1: arnoldi_fused_kernel<1><<<ARN_CLUSTER, ARN_THREADS, 0, c->stream>>>(c->V, m2, k, m, c->H, c->cs, c->sn, c->g, S, c->host_info_dev); break;
+      case 2: arnoldi_fused_kernel<2><<<ARN_CLUSTER, ARN_THREADS, 0, c->stream>>>(c->V, m2, k, m, c->H, c->cs, c->sn, c->g, S, c->host_info_dev); break;
+      case 4: arnoldi_fused_kernel<4><<<ARN_CLUSTER, ARN_THREADS, 0, c->stream>>>(c->V, m2, k, m, c->H, c->cs, c->sn, c->g, S, c->host_info_dev); break;
+      default: arnoldi_fused_kernel<8><<<ARN_CLUSTER, ARN_THREADS, 0, c->stream>>>(c->V, m2, k, m, c->H, c->cs, c->sn, c->g, S, c->host_info_dev); break;
+    }
+    c->launches_all++;
+    CK(cudaGetLastError());
+    if (!c->host_info_dev)
+      CK(cudaMemcpyAsync(c->host_info, S + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    return BIPB_OK;
+  }
   axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, c->stream>>>(w, nullptr, nullptr, c->V, m2, c->red_part, c->red_cnt,
                                                               c->H + 0 * m + k);
   c->launches_all++;
@@ -1525,6 +1557,8 @@ bipb_status bipb_set_matvec_kernel(bipb_ctx* c, int32_t kind) {
 }
 
 int32_t bipb_get_matvec_kernel(bipb_ctx* c) { return c ? c->mv_kind : -1; }
+
+int32_t bipb_get_arnoldi(bipb_ctx* c) { return c ? c->arn_E : -1; }
 
 int32_t bipb_get_exchange(bipb_ctx* c) {
   if (!c) return -1;

@@ -5,6 +5,7 @@
 // results are bitwise reproducible and identical on every rank.
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace bipb {
@@ -193,10 +194,9 @@ __global__ void init_g_kernel(double* g, const double* beta, int m) {
 
 // One Givens step on column k of H ((m+1) x m row-major), SURVEY.md §8(c) O4.
 // hk1sq = ||w||^2 after orthogonalisation. info[0] = |g_{k+1}| / beta_b, info[1] = h_{k+1,k}.
-__global__ void givens_kernel(double* H, double* cs, double* sn, double* g, const double* hk1sq, double* hk1,
-                              int k, int m, const double* beta_b_ptr, double* info) {
-  const double beta_b = *beta_b_ptr;
-  const double h = sqrt(*hk1sq);
+__device__ __forceinline__ void givens_step(double* H, double* cs, double* sn, double* g, double hk1sq, double* hk1,
+                                            int k, int m, double beta_b, double* info) {
+  const double h = sqrt(hk1sq);
   H[(k + 1) * m + k] = h;
   for (int i = 0; i < k; ++i) {
     const double a = H[i * m + k], c = H[(i + 1) * m + k];
@@ -214,6 +214,97 @@ __global__ void givens_kernel(double* H, double* cs, double* sn, double* g, cons
   *hk1 = h;
   info[0] = fabs(g[k + 1]) / beta_b;
   info[1] = h;
+}
+__global__ void givens_kernel(double* H, double* cs, double* sn, double* g, const double* hk1sq, double* hk1,
+                              int k, int m, const double* beta_b_ptr, double* info) {
+  givens_step(H, cs, sn, g, *hk1sq, hk1, k, m, *beta_b_ptr, info);
+}
+
+// ------------------------------------------------ fused Arnoldi tail on one thread-block cluster
+// For short Krylov vectors (2N <= ARN_CLUSTER * ARN_THREADS * E) the k + 2 dependent reductions
+// of one MGS sweep (h_0 = <w, v_0>; for i = 0..k: w -= h_i v_i,
+// h_{i+1} = <w, v_{i+1}> (i < k) or ||w||^2 (i = k)), the Givens step and w /= h_{k+1,k} run in ONE
+// kernel on ONE cluster instead of k + 4 launches: w and the current v_i stay in registers, each
+// CTA reduces its part (fixed shuffle tree), the cluster's CTA partials are exchanged through
+// distributed shared memory behind one cluster barrier per reduction and summed by every CTA in
+// rank order (bitwise the same total everywhere; deterministic, no atomics).  Same arithmetic per
+// element as axpy_dot_kernel / scale_div_kernel; only the summation order of the dots differs.
+// The residual record is also stored to `info_host` (pinned, device-mapped) when non-null.
+constexpr int ARN_THREADS = 1024;
+constexpr int ARN_CLUSTER = 8;  // portable cluster size
+template <int E>
+__global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREADS, 1)
+    arnoldi_fused_kernel(double* __restrict__ V, int64_t m2, int k, int m, double* H, double* cs, double* sn,
+                         double* g, double* S, double* info_host) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double ws[ARN_THREADS / 32];
+  __shared__ double cpart[2];
+  __shared__ double tot;
+  auto reduce = [&](double acc, int step) -> double {
+    acc = warp_sum(acc);
+    if (lane == 0) ws[warp] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      const double r = warp_sum(ws[lane]);
+      if (lane == 0) cpart[step & 1] = r;
+    }
+    cl.sync();  // every CTA's partial of this step is visible cluster-wide
+    if (warp == 0) {
+      double r = (lane < ARN_CLUSTER) ? *cl.map_shared_rank(&cpart[step & 1], lane) : 0.0;
+      r = warp_sum(r);
+      if (lane == 0) tot = r;
+    }
+    __syncthreads();
+    return tot;
+  };
+  double* wg = V + (int64_t)(k + 1) * m2;
+  double w[E], z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
+    w[e] = (t < m2) ? wg[t] : 0.0;
+    z[e] = (t < m2) ? V[t] : 0.0;  // v_0
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc = fma(w[e], z[e], acc);
+  double h = reduce(acc, 0);
+  const bool lead = (rank == 0 && threadIdx.x == 0);
+  if (lead) H[0 * m + k] = h;
+  for (int i = 0; i <= k; ++i) {
+    acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      w[e] = w[e] - h * z[e];  // z = v_i
+      if (i < k) {
+        const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
+        z[e] = (t < m2) ? V[(int64_t)(i + 1) * m2 + t] : 0.0;
+        acc = fma(w[e], z[e], acc);
+      } else {
+        acc = fma(w[e], w[e], acc);
+      }
+    }
+    h = reduce(acc, i + 1);
+    if (lead && i < k) H[(i + 1) * m + k] = h;
+  }
+  // h = ||w||^2: Givens on column k (one thread), then every thread normalises its elements
+  if (lead) {
+    givens_step(H, cs, sn, g, h, S + 3, k, m, S[0], S + 6);
+    if (info_host) {
+      info_host[0] = S[6];
+      info_host[1] = S[7];
+    }
+  }
+  const double hn = sqrt(h);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
+    if (t < m2) wg[t] = w[e] / hn;
+  }
+  cl.sync();  // no CTA exits while a peer may still read its shared memory
 }
 
 // back substitution H[0:k,0:k] y = g[0:k]

@@ -483,3 +483,31 @@ def test_full_size_c5_sampled_matvec(bp):
     y0 = bp.bipb_matvec(ctx, u)
     assert _rel(y, y0) <= 1e-13
     ctx.close()
+
+
+@pytest.mark.parametrize("keep", [4999, 30000])
+def test_fused_arnoldi_matches_launches(bp, keep, monkeypatch):
+    """The one-cluster Arnoldi kernel (bipb_get_arnoldi > 0: MGS dots reduced through distributed
+    shared memory) runs the same algorithm as the multi-launch MGS: same iterations, solutions
+    equal to rounding, and the mode follows the 2N <= 65536 rule (bipb.h)."""
+    p = _ragged(6 if keep > 20480 else 4, 4.0, keep, 3, g.charges_in_ball(25, 3.0, 4))
+    out = {}
+    for mode in ("fused", "launches"):
+        monkeypatch.setenv("BIPB_ARNOLDI", mode)
+        ctx = _ctx(bp, p)
+        out[mode] = (ctx.arnoldi,) + tuple(bp.solve(ctx, restart_m=10, tol=1e-10)[k] for k in ("x", "energy", "report"))
+        ctx.close()
+    ef = {4999: 2, 30000: 8}[keep]
+    assert out["fused"][0] == ef and out["launches"][0] == 0
+    assert out["fused"][3]["iterations"] == out["launches"][3]["iterations"]
+    assert _rel(out["fused"][1], out["launches"][1]) <= 1e-12
+    assert out["fused"][2] == pytest.approx(out["launches"][2], rel=1e-12)
+
+
+def test_fused_arnoldi_size_rule(bp):
+    q = g.charges_in_ball(5, 3.0, 2)
+    for keep, want in ((32768, 8), (32769, 0)):
+        p = _ragged(6, 4.0, keep, 5, q)
+        ctx = _ctx(bp, p)
+        assert ctx.arnoldi == want
+        ctx.close()
