@@ -22,6 +22,9 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+#include "bipb_kernels.cuh"
+
+
 #include "bipb_vec.cuh"
 
 namespace bipb {
@@ -56,6 +59,7 @@ __global__ void reduce_matvec_p2p_kernel(const double* __restrict__ part, int64_
   const int64_t off = static_cast<int64_t>(p2p_next_parity(epoch)) * stride;
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) {
       s0 += part[(2 * c) * ntgt + l];
       s1 += part[(2 * c + 1) * ntgt + l];
@@ -78,6 +82,7 @@ __global__ void reduce_source_p2p_kernel(const double* __restrict__ part, int64_
   const int64_t off = static_cast<int64_t>(p2p_next_parity(epoch)) * stride;
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) {
       s0 += part[(2 * c) * ntgt + l];
       s1 += part[(2 * c + 1) * ntgt + l];
@@ -98,6 +103,7 @@ __global__ void reduce_energy_p2p_kernel(const double* __restrict__ part, int64_
   const int64_t off = static_cast<int64_t>(p2p_next_parity(epoch)) * stride;
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) s0 += part[(2 * c) * ntgt + l];
     for (int p = 0; p < world; ++p) box.p[p][off + k0 + l] = s0;
   }

@@ -8,6 +8,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include "bipb_kernels.cuh"
+
 namespace bipb {
 
 constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
@@ -36,6 +38,7 @@ __global__ void reduce_matvec_kernel(const double* __restrict__ part, int64_t nc
                                      double d2, double* __restrict__ out0, double* __restrict__ out1) {
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) {
       s0 += part[(2 * c) * ntgt + l];
       s1 += part[(2 * c + 1) * ntgt + l];
@@ -50,6 +53,7 @@ __global__ void reduce_source_kernel(const double* __restrict__ part, int64_t nc
                                      double* __restrict__ out0, double* __restrict__ out1) {
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) {
       s0 += part[(2 * c) * ntgt + l];
       s1 += part[(2 * c + 1) * ntgt + l];
@@ -64,6 +68,7 @@ __global__ void reduce_energy_kernel(const double* __restrict__ part, int64_t nc
                                      double* __restrict__ out) {
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < ntgt; l += (int64_t)gridDim.x * blockDim.x) {
     double s0 = 0.0;
+#pragma unroll RED_UNROLL
     for (int64_t c = 0; c < nchunk; ++c) s0 += part[(2 * c) * ntgt + l];
     out[l] = s0;
   }
@@ -224,11 +229,14 @@ __global__ void givens_kernel(double* H, double* cs, double* sn, double* g, cons
 // For short Krylov vectors (2N <= ARN_CLUSTER * ARN_THREADS * E) the k + 2 dependent reductions
 // of one MGS sweep (h_0 = <w, v_0>; for i = 0..k: w -= h_i v_i,
 // h_{i+1} = <w, v_{i+1}> (i < k) or ||w||^2 (i = k)), the Givens step and w /= h_{k+1,k} run in ONE
-// kernel on ONE cluster instead of k + 4 launches: w and the current v_i stay in registers, each
-// CTA reduces its part (fixed shuffle tree), the cluster's CTA partials are exchanged through
-// distributed shared memory behind one cluster barrier per reduction and summed by every CTA in
-// rank order (bitwise the same total everywhere; deterministic, no atomics).  Same arithmetic per
-// element as axpy_dot_kernel / scale_div_kernel; only the summation order of the dots differs.
+// kernel on ONE cluster instead of k + 4 launches.  w and the current v_i stay in registers.  A
+// reduction: warp partials (fixed shuffle tree) -> CTA partial in shared memory -> one cluster
+// barrier -> warp 0 of every CTA reads the 8 CTA partials through distributed shared memory and
+// sums them in rank order: bitwise the same total in every CTA, deterministic, no atomics.  The
+// CTA-partial slot alternates by step parity, so one cluster barrier per reduction suffices.
+// (Measured at C1: letting every warp read all 8 x 32 warp partials instead of the second
+// __syncthreads is 15% slower; prefetching v_{i+1} one reduction ahead gains nothing.)  Same
+// arithmetic per element as axpy_dot_kernel / scale_div_kernel; only the dots' summation order differs.
 // The residual record is also stored to `info_host` (pinned, device-mapped) when non-null.
 constexpr int ARN_THREADS = 1024;
 constexpr int ARN_CLUSTER = 8;  // portable cluster size
@@ -237,6 +245,7 @@ __global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREAD
     arnoldi_fused_kernel(double* __restrict__ V, int64_t m2, int k, int m, double* H, double* cs, double* sn,
                          double* g, double* S, double* info_host) {
   namespace cg = cooperative_groups;
+  static_assert(ARN_THREADS / 32 == 32, "one warp partial per lane");
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -260,11 +269,12 @@ __global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREAD
     __syncthreads();
     return tot;
   };
+  auto idx = [&](int e) { return ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x; };
   double* wg = V + (int64_t)(k + 1) * m2;
   double w[E], z[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
+    const int64_t t = idx(e);
     w[e] = (t < m2) ? wg[t] : 0.0;
     z[e] = (t < m2) ? V[t] : 0.0;  // v_0
   }
@@ -280,8 +290,8 @@ __global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREAD
     for (int e = 0; e < E; ++e) {
       w[e] = w[e] - h * z[e];  // z = v_i
       if (i < k) {
-        const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
-        z[e] = (t < m2) ? V[(int64_t)(i + 1) * m2 + t] : 0.0;
+        const int64_t t = idx(e);
+        z[e] = (t < m2) ? V[(int64_t)(i + 1) * m2 + t] : 0.0;  // v_{i+1}
         acc = fma(w[e], z[e], acc);
       } else {
         acc = fma(w[e], w[e], acc);
@@ -301,7 +311,7 @@ __global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREAD
   const double hn = sqrt(h);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int64_t t = ((int64_t)e * ARN_CLUSTER + rank) * ARN_THREADS + threadIdx.x;
+    const int64_t t = idx(e);
     if (t < m2) wg[t] = w[e] / hn;
   }
   cl.sync();  // no CTA exits while a peer may still read its shared memory
