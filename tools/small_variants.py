@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "build", "small_variants")
 # (session 2 also timed two fused-Arnoldi reduction variants and a one-wave chunk rule for the row
 # kernel, since removed: profiles/r01/small_variants_C1.jsonl / _C2.jsonl)
-VARIANTS = {"default": [], "red_unroll1": ["-DBIPB_RED_UNROLL=1"]}
+VARIANTS = {"default": [], "red_unroll1": ["-DBIPB_RED_UNROLL=1"], "diag_branch": ["-DBIPB_DIAG_SELECT=0"]}
 
 
 def build():
