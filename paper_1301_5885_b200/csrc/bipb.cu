@@ -58,7 +58,15 @@ template <>
 struct SymCfg<4> {
   static constexpr int TPB = 128, T = 2, MINB = 1;
 };
+// R = 1 on mid-size problems (fewer than SYM_SMALL_TASKS block pairs at T = 5): smaller blocks,
+// 3 CTAs per SM -- more, shorter (I, J) tasks balance better over 148 SMs (measured: C2 product
+// 0.966 -> 0.863 ms; C3/C4 are faster at T = 5; profiles/r01/tune_shape_C*.jsonl)
+struct SymCfgMid {
+  static constexpr int TPB = 128, T = 3, MINB = 3;
+};
+constexpr int64_t SYM_SMALL_TASKS = 2048;
 static_assert((SymCfg<1>::TPB * SymCfg<1>::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
+static_assert((SymCfgMid::TPB * SymCfgMid::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
 constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
 constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
@@ -389,9 +397,13 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   bipb_ctx::SymPlan& p = c->sym[sym_slot(R)];
   *out = &p;
   if (p.R == R) return BIPB_OK;
-  constexpr int B = SymCfg<R>::TPB * SymCfg<R>::T;
   constexpr int F = SymLayout<R>::F;
   const int64_t n = c->n;
+  int64_t B = SymCfg<R>::TPB * SymCfg<R>::T;
+  if (R == 1) {
+    const int64_t nb5 = cdiv(n, B), h5 = (nb5 & 1) ? (nb5 - 1) / 2 : nb5 / 2;
+    if (nb5 * (h5 + 1) < SYM_SMALL_TASKS) B = SymCfgMid::TPB * SymCfgMid::T;
+  }
   p.B = B;
   p.nb = cdiv(n, B);
   p.hmax = (p.nb & 1) ? (p.nb - 1) / 2 : p.nb / 2;
@@ -445,7 +457,12 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
     if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
     cudaEvent_t stop;
     CKS(timed_begin(c, 0, &stop));
-    if (c->screened) {
+    if (R == 1 && p->B == SymCfgMid::TPB * SymCfgMid::T) {
+      using M = SymCfgMid;
+      auto k = c->screened ? sym_kernel<M::TPB, M::T, true, M::MINB, R> : sym_kernel<M::TPB, M::T, false, M::MINB, R>;
+      CKS(set_smem(k, smem));
+      k<<<(unsigned)grid, M::TPB, smem, c->stream>>>(a);
+    } else if (c->screened) {
       auto k = sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R>;
       CKS(set_smem(k, smem));
       k<<<(unsigned)grid, Cfg::TPB, smem, c->stream>>>(a);

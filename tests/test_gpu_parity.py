@@ -511,3 +511,24 @@ def test_fused_arnoldi_size_rule(bp):
         ctx = _ctx(bp, p)
         assert ctx.arnoldi == want
         ctx.close()
+
+
+@pytest.mark.parametrize("n_keep", [20000, 45001])
+def test_symmetric_block_shapes_ragged(bp, n_keep):
+    """Both R = 1 block shapes of the symmetric kernel on ragged sizes: N = 20,000 (mid-size
+    shape, B = 384: 53 blocks, 27 offsets, 1,431 tasks < 2,048) and N = 45,001 (B = 640: 71
+    blocks, 36 offsets, 2,556 tasks, partial last block).  Sampled rows (block edges included)
+    against the oracle, the whole product against the independently pinned row kernel."""
+    p = _ragged(6, 20.0, n_keep, 11, g.charges_in_ball(10, 15.0, 6))
+    ctx = _ctx(bp, p)
+    u = g.random_vector(2 * p.n, 5)
+    ctx.set_matvec_kernel(1)
+    y1 = bp.bipb_matvec(ctx, u)
+    ctx.set_matvec_kernel(0)
+    y0 = bp.bipb_matvec(ctx, u)
+    ctx.close()
+    assert _rel(y1, y0) <= 1e-13
+    rows = np.unique(np.array([0, 1, 383, 384, 639, 640, 767, 768, p.n // 2, p.n - 2, p.n - 1]))
+    yi, yin = oracle.matvec_rows(p, u, rows)
+    assert np.max(np.abs(y1[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
+    assert np.max(np.abs(y1[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))

@@ -15,9 +15,11 @@ OUT = os.path.join(ROOT, "build", "variants")
 VARIANTS = []
 # symmetric-kernel variants: launch shape (TPB * T a multiple of the 128-source smem tile) plus
 # extra -D macros ("defs")
-for defs in ({}, {"BIPB_RSQ_INT": 1}, {"BIPB_EXP_F32K": 1}, {"BIPB_RSQ_INT": 1, "BIPB_EXP_F32K": 1}):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3, "defs": defs})
+# (session 2: {"BIPB_RSQ_INT": 1}, {"BIPB_EXP_F32K": 1} and both measured slower at C4 —
+# profiles/r01/tune_int_variants_C4.jsonl; now: block-shape sweep for mid-size problems)
+for t, minb in ((5, 1), (4, 1), (3, 1), (3, 3), (2, 4)):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
+                     "tile": 128, "stages": 3, "defs": {}})
 
 
 def name(v):
