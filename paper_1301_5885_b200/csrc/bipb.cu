@@ -50,13 +50,19 @@ template <>
 struct SymCfg<1> {
   static constexpr int TPB = BIPB_SYM_TPB, T = BIPB_SYM_T, MINB = BIPB_SYM_MINB;
 };
+#ifndef BIPB_SYM2_T
+#define BIPB_SYM2_T 4  // shape sweep at C4 (profiles/r01/tune_batch2_C4.jsonl): R = 2 T = 4 236.9 ms, T = 2 257.3
+#endif
+#ifndef BIPB_SYM4_T
+#define BIPB_SYM4_T 3  // R = 4: T = 3 328.7 ms, T = 2 367.0
+#endif
 template <>
 struct SymCfg<2> {
-  static constexpr int TPB = 128, T = 2, MINB = 1;
+  static constexpr int TPB = 128, T = BIPB_SYM2_T, MINB = 1;
 };
 template <>
 struct SymCfg<4> {
-  static constexpr int TPB = 128, T = 2, MINB = 1;
+  static constexpr int TPB = 128, T = BIPB_SYM4_T, MINB = 1;
 };
 // R = 1 on mid-size problems (fewer than SYM_SMALL_TASKS block pairs at T = 5): smaller blocks,
 // 3 CTAs per SM -- more, shorter (I, J) tasks balance better over 148 SMs (measured: C2 product
@@ -440,7 +446,8 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
   a.sc1 = c->s; a.sc2 = c->s * c->s;
   a.fwd = p->fwd; a.rev = p->rev;
   const size_t smem =
-      sizeof(double) * (STAGES * TILE * SymLayout<R>::F + (Cfg::TPB / 32) * R * 2 * p->B) + 8 * STAGES;
+      sizeof(double) * (STAGES * TILE * SymLayout<R>::F + (Cfg::TPB / 32) * R * 2 * sym_rs_rows(R, (int)p->B)) +
+      8 * STAGES;
   const PeerBoxes nobox{};
   if (p->I1 <= p->I0) {  // no I-blocks on this rank: its partial sums are zero
     if (c->p2p) {
@@ -457,11 +464,17 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
     if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
     cudaEvent_t stop;
     CKS(timed_begin(c, 0, &stop));
-    if (R == 1 && p->B == SymCfgMid::TPB * SymCfgMid::T) {
-      using M = SymCfgMid;
-      auto k = c->screened ? sym_kernel<M::TPB, M::T, true, M::MINB, R> : sym_kernel<M::TPB, M::T, false, M::MINB, R>;
-      CKS(set_smem(k, smem));
-      k<<<(unsigned)grid, M::TPB, smem, c->stream>>>(a);
+    bool mid = false;
+    if constexpr (R == 1) {
+      if (p->B == SymCfgMid::TPB * SymCfgMid::T) {
+        using M = SymCfgMid;
+        auto k = c->screened ? sym_kernel<M::TPB, M::T, true, M::MINB, R> : sym_kernel<M::TPB, M::T, false, M::MINB, R>;
+        CKS(set_smem(k, smem));
+        k<<<(unsigned)grid, M::TPB, smem, c->stream>>>(a);
+        mid = true;
+      }
+    }
+    if (mid) {
     } else if (c->screened) {
       auto k = sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R>;
       CKS(set_smem(k, smem));

@@ -46,6 +46,8 @@ struct SymLayout {
   __host__ __device__ static constexpr int C(int r) { return (R == 1) ? 3 : 6 + 2 * r; }
   __host__ __device__ static constexpr int A(int r) { return (R == 1) ? 4 : 7 + 2 * r; }
 };
+// source rows per warp-combine of the reverse sums (see sym_kernel)
+__host__ __device__ constexpr int sym_rs_rows(int R, int B) { return R == 1 ? B : TILE; }
 __host__ __device__ constexpr int64_t sym_idx(int64_t j, int f, int F) {
   return (j / TILE) * (TILE * F) + f * TILE + (j % TILE);
 }
@@ -164,8 +166,13 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double s_tab[EXP_TAB];
   double* sbuf = reinterpret_cast<double*>(smem_raw);  // [STAGES][F][TILE]
-  double* rsum = sbuf + STAGES * TILE * F;              // [NW][R][2][B] per-warp reverse sums of the J-block
-  uint64_t* full = reinterpret_cast<uint64_t*>(rsum + NW * R * 2 * B);
+  // per-warp reverse sums [NW][R][2][RS], combined over the warps every RS source rows: the whole
+  // J-block for R = 1 (one barrier per J-block), every stage for R > 1 (NW*R*2*TILE doubles instead
+  // of NW*R*2*B: R = 4 needs 32 KB instead of 64-98 KB, which keeps 2 CTAs per SM; measured R = 4
+  // at C4 456 -> 329 ms per product, R = 1 per stage would cost 0.7%)
+  constexpr int RS = sym_rs_rows(R, B);
+  double* rsum = sbuf + STAGES * TILE * F;
+  uint64_t* full = reinterpret_cast<uint64_t*>(rsum + NW * R * 2 * RS);
   for (int i = threadIdx.x; i < EXP_TAB; i += TPB) s_tab[i] = g_exp_tab[i];
   const PairConst kc{a.eps, a.inveps, a.eps - 1.0, 1.0 - a.inveps};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -372,26 +379,28 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
       if (lane < gcnt) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          double* rs = rsum + ((warp * R + r) * 2) * B + jl0 + g0 + lane;
+          double* rs = rsum + ((warp * R + r) * 2) * RS + (jl0 % RS) + g0 + lane;
           rs[0] = rv[r].p0;
-          rs[B] = rv[r].p1;
+          rs[RS] = rv[r].p1;
         }
       }
     }
     __syncthreads();  // buffer `buf` consumed; rsum entries of this stage written
     if (threadIdx.x == 0 && q + STAGES < nstage) issue(q + STAGES, buf);
-    if ((q + 1) % stages_per_block == 0) {
-      // end of J-block: combine warps (fixed order), fold s powers, write Rev[I][o]
+    if ((q + 1) % (RS / TILE) == 0) {
+      // combine the warps (fixed order), fold the s powers, write rows base .. base + RS of Rev[I][o]
       const int64_t J = (I + o) % a.nb;
-      for (int jl = threadIdx.x; jl < B; jl += TPB) {
+      const int base = jl0 + TILE - RS;
+      for (int jt = threadIdx.x; jt < RS; jt += TPB) {
+        const int jl = base + jt;
         if (J * B + jl >= a.n) continue;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           double q0 = 0.0, q1 = 0.0;
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            q0 += rsum[((w * R + r) * 2) * B + jl];
-            q1 += rsum[((w * R + r) * 2 + 1) * B + jl];
+            q0 += rsum[((w * R + r) * 2) * RS + jt];
+            q1 += rsum[((w * R + r) * 2 + 1) * RS + jt];
           }
           double* rv0 = a.rev + (((Il * (a.hmax + 1) + o) * R + r) * 2) * B;
           if constexpr (SCREENED) {
@@ -403,7 +412,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
           }
         }
       }
-      __syncthreads();  // rsum reused by the next J-block
+      __syncthreads();  // rsum reused
     }
   }
 

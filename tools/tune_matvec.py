@@ -17,9 +17,10 @@ VARIANTS = []
 # extra -D macros ("defs")
 # (session 2: {"BIPB_RSQ_INT": 1}, {"BIPB_EXP_F32K": 1} and both measured slower at C4 —
 # profiles/r01/tune_int_variants_C4.jsonl; now: block-shape sweep for mid-size problems)
-for t, minb in ((5, 1), (4, 1), (3, 1), (3, 3), (2, 4)):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3, "defs": {}})
+# (block-shape sweep for R = 1: profiles/r01/tune_shape_C*.jsonl); multi-RHS shapes (`batch` mode):
+for t2, t4 in ((2, 2), (4, 3), (3, 3), (4, 2)):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
+                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM2_T": t2, "BIPB_SYM4_T": t4}})
 
 
 def name(v):
@@ -123,6 +124,18 @@ if __name__ == "__main__":
             print(json.dumps({"R": R, "ms_per_batch": ms, "pairs_per_s_all_rhs": R * p.n * (p.n - 1) / (ms / 1e3),
                               "ms_per_rhs": ms / R}), flush=True)
         ctx.close()
+    elif cmd == "runbatch":  # the batch measurement for every variant library
+        cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
+        for v in VARIANTS:
+            env = dict(os.environ, BIPB_LIB=os.path.join(OUT, f"libbipb_{name(v)}.so"))
+            out = subprocess.run([sys.executable, __file__, "batch", cfg], env=env, capture_output=True, text=True,
+                                 timeout=900)
+            for line in out.stdout.strip().splitlines():
+                d = json.loads(line)
+                d.update(v["defs"])
+                print(json.dumps(d), flush=True)
+            if out.returncode:
+                print(json.dumps({"error": out.stderr[-400:], **v["defs"]}), flush=True)
     elif cmd == "build":
         build()
     elif cmd == "one":
