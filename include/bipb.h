@@ -222,6 +222,21 @@ int32_t bipb_get_exchange(bipb_ctx* ctx);
 int32_t bipb_get_arnoldi(bipb_ctx* ctx);
 
 /*
+ * GMRES preconditioning (NOT in the paper, which runs plain GMRES; default 0):
+ *   0  plain GMRES(m) (the paper's method; parity with the oracle's iteration counts)
+ *   1  right preconditioning by the diagonal of the jump terms of Eqs. (12)-(13),
+ *      M = diag(1/2 (1 + eps) I_N, 1/2 (1 + 1/eps) I_N) (Saad, Algorithm 9.5: each Arnoldi step
+ *      applies A to M^-1 v_k; a cycle ends with x += M^-1 V y).  Same linear system and the same
+ *      true-residual test ||b - A x|| / ||b|| <= tol, so the same solution and energy to the
+ *      tolerance; the 40.5 : 0.506 scaling of the two row blocks (eps = 80) no longer slows the
+ *      Krylov iteration (C4: 26 -> 11 iterations).  Applies to bipb_gmres_solve and
+ *      bipb_gmres_solve_batch.  BIPB_PRECOND=jacobi in the environment sets 1 at setup.
+ * ERR_ARG for a NULL context or another kind; bipb_get_precond returns -1 for a NULL context.
+ */
+bipb_status bipb_set_precond(bipb_ctx* ctx, int32_t kind);
+int32_t bipb_get_precond(bipb_ctx* ctx);
+
+/*
  * Instrumentation (bench.py, tests).  `which`: 0 = matvec pair kernel, 1 = source pair
  * kernel, 2 = energy pair kernel, 3 = all kernels of the library.
  * bipb_timing_enable(ctx, 1) brackets each pair-kernel launch with CUDA events on the

@@ -57,6 +57,8 @@ def lib():
             ("orc_dense_assemble", [i, p, p, p, d, d, p], None),
             ("orc_gmres_dense", [i, p, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
             ("orc_gmres_bem", [i, p, p, p, d, d, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
+            ("orc_gmres_dense_prec", [i, p, p, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
+            ("orc_gmres_bem_jacobi", [i, p, p, p, d, d, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
             ("orc_reaction_potential", [i, p, p, p, d, d, i, p, p, p], None),
             ("orc_energy", [i, p, p, p, d, d, i, p, p, p], d),
         ]:
@@ -160,25 +162,33 @@ def _report(rep, hist):
             "rel_res_true": rep.rel_res_true, "history": hist[:min(rep.history_len, hist.size)].copy()}
 
 
-def gmres_dense(A, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True):
+def gmres_dense(A, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True, minv=None):
+    """minv: right preconditioner M = diag(1 / minv) (Saad Alg. 9.5), None = plain GMRES."""
     A, b = _c(A), _c(b)
     m = b.size
     x = np.zeros(m) if x0 is None else _c(x0).copy()
     hist = np.zeros(max_iters + 1)
     rep = Report(history=_p(hist), history_cap=hist.size)
-    st = lib().orc_gmres_dense(m, _p(A), _p(b), _p(x), restart, tol, max_iters, int(check_true),
-                               ctypes.byref(rep))
+    if minv is None:
+        st = lib().orc_gmres_dense(m, _p(A), _p(b), _p(x), restart, tol, max_iters, int(check_true),
+                                   ctypes.byref(rep))
+    else:
+        st = lib().orc_gmres_dense_prec(m, _p(A), _p(b), _p(x), _p(_c(minv)), restart, tol, max_iters,
+                                        int(check_true), ctypes.byref(rep))
     return x, st, _report(rep, hist)
 
 
-def gmres(prob, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True):
+def gmres(prob, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=True, precond=False):
+    """precond=True: right preconditioning by the jump-term diagonal (orc_gmres_bem_jacobi; not in
+    the paper, the library's opt-in bipb_set_precond(ctx, 1))."""
     b = _c(b)
     x = np.zeros(2 * prob.n) if x0 is None else _c(x0).copy()
     hist = np.zeros(max_iters + 1)
     rep = Report(history=_p(hist), history_cap=hist.size)
-    st = lib().orc_gmres_bem(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
-                             eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(b), _p(x), restart, tol,
-                             max_iters, int(check_true), ctypes.byref(rep))
+    fn = lib().orc_gmres_bem_jacobi if precond else lib().orc_gmres_bem
+    st = fn(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
+            eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(b), _p(x), restart, tol,
+            max_iters, int(check_true), ctypes.byref(rep))
     return x, st, _report(rep, hist)
 
 
@@ -197,9 +207,9 @@ def energy(prob, x) -> float:
                             _p(_c(x)), None)
 
 
-def solve(prob, restart=20, tol=1e-10, max_iters=500, check_true=True):
+def solve(prob, restart=20, tol=1e-10, max_iters=500, check_true=True, precond=False):
     """Table 1 pipeline: source -> GMRES -> energy.  Returns a dict."""
     b = source(prob)
-    x, st, rep = gmres(prob, b, None, restart, tol, max_iters, check_true)
+    x, st, rep = gmres(prob, b, None, restart, tol, max_iters, check_true, precond)
     e = energy(prob, x)
     return {"b": b, "x": x, "status": st, "report": rep, "energy": e}

@@ -193,9 +193,13 @@ static double dotv(int64_t m, const double* a, const double* b) {
   return s;
 }
 
-/* Solve op(x) = b for x (length m); x holds x0 on entry. Returns 0 converged, 2 not. */
+/* Solve op(x) = b for x (length m); x holds x0 on entry. Returns 0 converged, 2 not.
+ * minv != NULL: right-preconditioned GMRES with M = diag(1 / minv) (Saad, Iterative Methods for
+ * Sparse Linear Systems, Algorithm 9.5): z_k = M^-1 v_k, w = op(z_k), ...; x = x0 + M^-1 (V y).
+ * The residual the convergence test uses is still b - op(x) (right preconditioning leaves it
+ * unchanged).  minv == NULL: plain GMRES as the paper. */
 static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, double* x, int64_t restart,
-                      double tol, int64_t max_iters, int64_t check_true, orc_report* rep) {
+                      double tol, int64_t max_iters, int64_t check_true, const double* minv, orc_report* rep) {
   double* V = (double*)malloc(sizeof(double) * (size_t)(m * (restart + 1)));
   double* H = (double*)calloc((size_t)((restart + 1) * restart), sizeof(double)); /* H[i*restart+k] */
   double* cs = (double*)calloc((size_t)restart, sizeof(double));
@@ -203,6 +207,7 @@ static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, doubl
   double* g = (double*)calloc((size_t)(restart + 1), sizeof(double));
   double* yv = (double*)calloc((size_t)restart, sizeof(double));
   double* r = (double*)malloc(sizeof(double) * (size_t)m);
+  double* z = minv ? (double*)malloc(sizeof(double) * (size_t)m) : NULL;
   int64_t its = 0, restarts = 0, matvecs = 0, converged = 0, hl = 0;
   double rel = 1.0;
   double beta_b = nrm2(m, b);
@@ -211,7 +216,7 @@ static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, doubl
     for (int64_t i = 0; i < m; ++i) x[i] = 0.0;
     rep->iterations = 0; rep->restarts = 0; rep->matvecs = 0; rep->converged = 1;
     rep->rel_res_est = 0.0; rep->rel_res_true = 0.0; rep->history_len = 0;
-    free(V); free(H); free(cs); free(sn); free(g); free(yv); free(r);
+    free(V); free(H); free(cs); free(sn); free(g); free(yv); free(r); free(z);
     return 0;
   }
   int first_cycle = 1;
@@ -239,7 +244,12 @@ static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, doubl
     int stop = 0;
     for (k = 0; k < restart; ++k) {
       double* w = V + (k + 1) * m;
-      op(ctx, V + k * m, w);
+      if (minv) {
+        for (int64_t t = 0; t < m; ++t) z[t] = minv[t] * V[k * m + t];
+        op(ctx, z, w);
+      } else {
+        op(ctx, V + k * m, w);
+      }
       ++matvecs;
       ++its;
       for (int64_t i = 0; i <= k; ++i) { /* modified Gram-Schmidt */
@@ -277,8 +287,16 @@ static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, doubl
       for (int64_t j = i + 1; j < kdone; ++j) s -= H[i * restart + j] * yv[j];
       yv[i] = s / H[i * restart + i];
     }
-    for (int64_t j = 0; j < kdone; ++j)
-      for (int64_t t = 0; t < m; ++t) x[t] += yv[j] * V[j * m + t];
+    if (minv) { /* x += M^-1 (V y) */
+      for (int64_t t = 0; t < m; ++t) {
+        double s = 0.0;
+        for (int64_t j = 0; j < kdone; ++j) s += yv[j] * V[j * m + t];
+        x[t] += minv[t] * s;
+      }
+    } else {
+      for (int64_t j = 0; j < kdone; ++j)
+        for (int64_t t = 0; t < m; ++t) x[t] += yv[j] * V[j * m + t];
+    }
     if (rel <= tol) { converged = 1; break; }
     if (its >= max_iters) break;
   }
@@ -294,7 +312,7 @@ static int gmres_core(orc_op_fn op, void* ctx, int64_t m, const double* b, doubl
   rep->converged = converged;
   rep->rel_res_est = rel;
   rep->history_len = hl;
-  free(V); free(H); free(cs); free(sn); free(g); free(yv); free(r);
+  free(V); free(H); free(cs); free(sn); free(g); free(yv); free(r); free(z);
   return converged ? 0 : 2;
 }
 
@@ -311,7 +329,13 @@ static void dense_op(void* vctx, const double* x, double* y) {
 int orc_gmres_dense(int64_t m, const double* A, const double* b, double* x, int64_t restart, double tol,
                     int64_t max_iters, int64_t check_true, orc_report* rep) {
   dense_ctx c = {m, A};
-  return gmres_core(dense_op, &c, m, b, x, restart, tol, max_iters, check_true, rep);
+  return gmres_core(dense_op, &c, m, b, x, restart, tol, max_iters, check_true, NULL, rep);
+}
+/* The same with right preconditioning M = diag(1 / minv). */
+int orc_gmres_dense_prec(int64_t m, const double* A, const double* b, double* x, const double* minv,
+                         int64_t restart, double tol, int64_t max_iters, int64_t check_true, orc_report* rep) {
+  dense_ctx c = {m, A};
+  return gmres_core(dense_op, &c, m, b, x, restart, tol, max_iters, check_true, minv, rep);
 }
 
 typedef struct {
@@ -326,7 +350,23 @@ int orc_gmres_bem(int64_t n, const double* cen, const double* nrm, const double*
                   double kappa, const double* b, double* x, int64_t restart, double tol, int64_t max_iters,
                   int64_t check_true, orc_report* rep) {
   bem_ctx c = {n, cen, nrm, area, eps, kappa};
-  return gmres_core(bem_op, &c, 2 * n, b, x, restart, tol, max_iters, check_true, rep);
+  return gmres_core(bem_op, &c, 2 * n, b, x, restart, tol, max_iters, check_true, NULL, rep);
+}
+/* GMRES on the BEM operator, right-preconditioned by the diagonal of the jump terms of
+ * Eqs. (12)-(13): M = diag(1/2 (1 + eps) I_N, 1/2 (1 + 1/eps) I_N) (not in the paper; the
+ * library's opt-in bipb_set_precond(ctx, 1)).  Same linear system, same residual test. */
+int orc_gmres_bem_jacobi(int64_t n, const double* cen, const double* nrm, const double* area, double eps,
+                         double kappa, const double* b, double* x, int64_t restart, double tol, int64_t max_iters,
+                         int64_t check_true, orc_report* rep) {
+  bem_ctx c = {n, cen, nrm, area, eps, kappa};
+  double* minv = (double*)malloc(sizeof(double) * (size_t)(2 * n));
+  for (int64_t i = 0; i < n; ++i) {
+    minv[i] = 1.0 / (0.5 * (1.0 + eps));
+    minv[n + i] = 1.0 / (0.5 * (1.0 + 1.0 / eps));
+  }
+  int st = gmres_core(bem_op, &c, 2 * n, b, x, restart, tol, max_iters, check_true, minv, rep);
+  free(minv);
+  return st;
 }
 
 /* ---------------------- Eq. (14): phi_reac(x_k) and E_sol (reading R3) */

@@ -76,6 +76,8 @@ _SIGS = {
     "bipb_get_matvec_kernel": ([_P], _I32),
     "bipb_get_exchange": ([_P], _I32),
     "bipb_get_arnoldi": ([_P], _I32),
+    "bipb_set_precond": ([_P, _I32], _I32),
+    "bipb_get_precond": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_a, _r) in _SIGS.items():
@@ -165,6 +167,14 @@ class Context:
     def exchange(self) -> str:
         """How products are exchanged between ranks: "none", "nccl" or "p2p" (peer stores)."""
         return {0: "none", 1: "nccl", 2: "p2p"}[int(_lib.bipb_get_exchange(self.handle))]
+
+    # GMRES preconditioning: 0 = plain (the paper), 1 = right jump-term diagonal (bipb.h) -------
+    def set_precond(self, kind: int):
+        _check(_lib.bipb_set_precond(self.handle, int(kind)))
+
+    @property
+    def precond(self) -> int:
+        return int(_lib.bipb_get_precond(self.handle))
 
     @property
     def arnoldi(self) -> int:
@@ -316,6 +326,15 @@ def bipb_get_matvec_kernel(ctx: Context) -> int:
 def bipb_get_exchange(ctx: Context) -> int:
     """0 none, 1 NCCL collectives, 2 peer stores (bipb.h)."""
     return int(_lib.bipb_get_exchange(ctx.handle))
+
+
+def bipb_set_precond(ctx: Context, kind: int):
+    """0 = plain GMRES (the paper), 1 = right preconditioning by the jump-term diagonal (bipb.h)."""
+    ctx.set_precond(kind)
+
+
+def bipb_get_precond(ctx: Context) -> int:
+    return ctx.precond
 
 
 def bipb_get_arnoldi(ctx: Context) -> int:

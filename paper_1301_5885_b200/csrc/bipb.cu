@@ -183,6 +183,9 @@ struct bipb_ctx {
   double* host_info = nullptr;  // pinned [4]
   double* host_info_dev = nullptr;  // its device mapping (UVA), or null
   int arn_E = -1;                   // fused Arnoldi tail: elements per thread (0 = multi-launch MGS)
+  int precond = 0;                  // 0 plain GMRES (paper), 1 right jump-term diagonal (bipb_set_precond)
+  double pinv1 = 1.0, pinv2 = 1.0;  // M^-1 on the phi / dphi rows
+  double* zbuf = nullptr;           // M^-1 v_k (2n)
   int* dflag = nullptr;
 
   // symmetric matvec (bipb_sym.cuh): one schedule per R in {1, 2, 4}
@@ -215,7 +218,7 @@ struct bipb_ctx {
   // CUDA graphs of the GMRES Arnoldi steps (one per k), valid for (V, m, n, kind)
   struct {
     const double* V = nullptr;
-    int m = 0, kind = -1;
+    int m = 0, kind = -1, precond = -1;
     std::vector<cudaGraphExec_t> ex;
   } ag;
 };
@@ -631,7 +634,7 @@ void bipb_destroy(bipb_ctx* c) {
   double* bufs[] = {c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->ew, c->rec_el, c->qx, c->qy, c->qz, c->q4,
                     c->rec_ch, c->part, c->b, c->stage, c->gather, c->ubuf, c->ybuf, c->xbuf, c->bbuf, c->tbuf,
                     c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part,
-                    c->sym_P, c->bat_U, c->bat_Y};
+                    c->sym_P, c->bat_U, c->bat_Y, c->zbuf};
   for (double* p : bufs)
     if (p) dfree(c, p);
   for (auto& sp : c->sym) {
@@ -841,6 +844,9 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   tr.mark("fetch + validate");
   c->n = n; c->nc = nc; c->eps1 = eps1; c->eps2 = eps2; c->kappa = kappa;
   c->eps = eps2 / eps1;  // reading R1
+  c->pinv1 = 1.0 / (0.5 * (1.0 + c->eps));  // opt-in right preconditioner M^-1 (bipb_set_precond)
+  c->pinv2 = 1.0 / (0.5 * (1.0 + 1.0 / c->eps));
+  if (const char* pe = getenv("BIPB_PRECOND")) c->precond = (!strcmp(pe, "jacobi") || !strcmp(pe, "1")) ? 1 : 0;
   c->screened = kappa > 0.0;
   c->s = c->screened ? kappa : 1.0;
   c->rank = dist ? dist->rank : 0;
@@ -1072,6 +1078,7 @@ static bipb_status ensure_krylov(bipb_ctx* c, int m) {
   CK(dmalloc(c, &c->sn, (size_t)m * sizeof(double)));
   CK(dmalloc(c, &c->g, (size_t)(m + 1) * sizeof(double)));
   CK(dmalloc(c, &c->yk, (size_t)m * sizeof(double)));
+  if (!c->zbuf) CK(dmalloc(c, &c->zbuf, (size_t)2 * c->n * sizeof(double)));
   c->m_cap = m;
   return BIPB_OK;
 }
@@ -1086,7 +1093,12 @@ static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
   double* S = c->scal;
   double* vk = c->V + (int64_t)k * m2;
   double* w = c->V + (int64_t)(k + 1) * m2;
-  CKS(matvec_dev(c, vk, w));
+  if (c->precond) {  // right preconditioning: w = A M^-1 v_k
+    LAUNCH1D(jacobi_scale_kernel, m2, c->zbuf, vk, c->n, c->pinv1, c->pinv2);
+    CKS(matvec_dev(c, c->zbuf, w));
+  } else {
+    CKS(matvec_dev(c, vk, w));
+  }
   if (c->arn_E > 0) {  // MGS + Givens + normalisation in one cluster kernel (bipb_vec.cuh)
     switch (c->arn_E) {
       case 1: arnoldi_fused_kernel<1><<<ARN_CLUSTER, ARN_THREADS, 0, c->stream>>>(c->V, m2, k, m, c->H, c->cs, c->sn, c->g, S, c->host_info_dev); break;
@@ -1126,13 +1138,14 @@ static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
   static const bool graphs_on = getenv("BIPB_GRAPHS") && !strcmp(getenv("BIPB_GRAPHS"), "1");
   const bool use = graphs_on && !c->timing && c->warm_kind == c->mv_kind;
   if (use) {
-    if (c->ag.V != c->V || c->ag.m != m || c->ag.kind != c->mv_kind) {
+    if (c->ag.V != c->V || c->ag.m != m || c->ag.kind != c->mv_kind || c->ag.precond != c->precond) {
       for (auto e : c->ag.ex)
         if (e) cudaGraphExecDestroy(e);
       c->ag.ex.assign(m, nullptr);
       c->ag.V = c->V;
       c->ag.m = m;
       c->ag.kind = c->mv_kind;
+      c->ag.precond = c->precond;
     }
     if (!c->ag.ex[k]) {
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1220,11 +1233,16 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
     }
   }
   // batched A applied to the listed systems' vectors src(q) -> dst(q)
-  auto apply = [&](std::vector<int>& list, auto src, auto dst) -> bipb_status {
+  auto apply = [&](std::vector<int>& list, auto src, auto dst, bool arnoldi = false) -> bipb_status {
     const int k = (int)list.size();
     if (k == 0) return BIPB_OK;
-    for (int t = 0; t < k; ++t)
-      CK(cudaMemcpyAsync(U + t * m2, src(sy[list[t]]), m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    for (int t = 0; t < k; ++t) {
+      if (arnoldi && c->precond) {  // right preconditioning: the operand is M^-1 v_k
+        LAUNCH1D(jacobi_scale_kernel, m2, U + t * m2, src(sy[list[t]]), c->n, c->pinv1, c->pinv2);
+      } else {
+        CK(cudaMemcpyAsync(U + t * m2, src(sy[list[t]]), m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
     CKS(matvec_batch_dev(c, k, U, Y));
     for (int t = 0; t < k; ++t) {
       CK(cudaMemcpyAsync(dst(sy[list[t]]), Y + t * m2, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1271,7 +1289,7 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
     // ---- Arnoldi steps in lockstep
     for (int k = 0; k < m && !iter.empty(); ++k) {
       CKS(apply(iter, [k, m2](GmresSys& q) { return (const double*)(q.V + (int64_t)k * m2); },
-                [k, m2](GmresSys& q) { return q.V + (int64_t)(k + 1) * m2; }));
+                [k, m2](GmresSys& q) { return q.V + (int64_t)(k + 1) * m2; }, true));
       std::vector<int> next;
       for (int r : iter) {
         GmresSys& q = sy[r];
@@ -1309,7 +1327,10 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
       q.in_cycle = false;
       backsolve_kernel<<<1, 1, 0, c->stream>>>(q.H, q.g, q.yk, q.kdone, m);
       c->launches_all++;
-      LAUNCH1D(update_x_kernel, m2, q.x, q.V, q.yk, q.kdone, m2);
+      if (c->precond)
+        LAUNCH1D(update_x_prec_kernel, m2, q.x, q.V, q.yk, q.kdone, c->n, c->pinv1, c->pinv2);
+      else
+        LAUNCH1D(update_x_kernel, m2, q.x, q.V, q.yk, q.kdone, m2);
       if (q.rel <= tol) q.converged = q.finished = true;
       else if (q.its >= max_iters) q.finished = true;
     }
@@ -1414,7 +1435,10 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
       }
       backsolve_kernel<<<1, 1, 0, c->stream>>>(c->H, c->g, c->yk, kdone, m);
       c->launches_all++;
-      LAUNCH1D(update_x_kernel, m2, xd, c->V, c->yk, kdone, m2);
+      if (c->precond)
+        LAUNCH1D(update_x_prec_kernel, m2, xd, c->V, c->yk, kdone, c->n, c->pinv1, c->pinv2);
+      else
+        LAUNCH1D(update_x_kernel, m2, xd, c->V, c->yk, kdone, m2);
       if (rel <= tol) { converged = true; break; }
       if (its >= max_iters) break;
     }
@@ -1589,6 +1613,14 @@ bipb_status bipb_set_matvec_kernel(bipb_ctx* c, int32_t kind) {
 int32_t bipb_get_matvec_kernel(bipb_ctx* c) { return c ? c->mv_kind : -1; }
 
 int32_t bipb_get_arnoldi(bipb_ctx* c) { return c ? c->arn_E : -1; }
+
+bipb_status bipb_set_precond(bipb_ctx* c, int32_t kind) {
+  if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  if (kind != 0 && kind != 1) return fail(BIPB_ERR_ARG, "precond kind must be 0 (none) or 1 (jump-term diagonal)");
+  c->precond = kind;
+  return BIPB_OK;
+}
+int32_t bipb_get_precond(bipb_ctx* c) { return c ? c->precond : -1; }
 
 int32_t bipb_get_exchange(bipb_ctx* c) {
   if (!c) return -1;

@@ -317,6 +317,26 @@ __global__ void __cluster_dims__(ARN_CLUSTER, 1, 1) __launch_bounds__(ARN_THREAD
   cl.sync();  // no CTA exits while a peer may still read its shared memory
 }
 
+// ---------------------------------------- right preconditioning by the jump-term diagonal (opt-in)
+// M = diag(1/2 (1 + eps) I_N, 1/2 (1 + 1/eps) I_N), s1 = M^-1 on the phi rows, s2 on the dphi rows
+// (bipb_set_precond; Saad Alg. 9.5: z_k = M^-1 v_k before the product, x += M^-1 (V y) at the end
+// of a cycle).  dst = M^-1 src
+__global__ void jacobi_scale_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n, double s1,
+                                    double s2) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 2 * n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = ((t < n) ? s1 : s2) * src[t];
+}
+// x += M^-1 (V[0:k] y)  (per element: the combination j ascending, then the scaling, as the oracle)
+__global__ void update_x_prec_kernel(double* __restrict__ x, const double* __restrict__ V,
+                                     const double* __restrict__ y, int k, int64_t n, double s1, double s2) {
+  const int64_t m = 2 * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s = s + y[j] * V[(int64_t)j * m + t];
+    x[t] = x[t] + ((t < n) ? s1 : s2) * s;
+  }
+}
+
 // back substitution H[0:k,0:k] y = g[0:k]
 __global__ void backsolve_kernel(const double* H, const double* g, double* y, int k, int m) {
   for (int i = k - 1; i >= 0; --i) {

@@ -532,3 +532,85 @@ def test_symmetric_block_shapes_ragged(bp, n_keep):
     yi, yin = oracle.matvec_rows(p, u, rows)
     assert np.max(np.abs(y1[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
     assert np.max(np.abs(y1[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))
+
+
+# ---- opt-in right preconditioning by the jump-term diagonal (bipb_set_precond; not in the paper) ----
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("name,make", CASES)
+def test_solve_parity_precond(bp, name, make, kind):
+    """GPU right-preconditioned GMRES against the oracle's (orc_gmres_bem_jacobi, pinned by its own
+    CPU tests): iterations +-1, energy 1e-8, x 1e-8; the energy also equals the plain solve's."""
+    p = make(g.KAPPA)
+    ref = oracle.solve(p, restart=20, tol=1e-10, precond=True)
+    plain = oracle.solve(p, restart=20, tol=1e-10)
+    ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(kind)
+    ctx.set_precond(1)
+    assert ctx.precond == 1
+    x = np.zeros(2 * p.n)
+    bp.bipb_source(ctx)
+    st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 500, check_true=True)
+    e = bp.bipb_energy(ctx, x)
+    ctx.close()
+    assert st == bp.OK and rep["converged"] and rep["rel_res_true"] <= 1e-9
+    assert abs(rep["iterations"] - ref["report"]["iterations"]) <= 1
+    assert e == pytest.approx(ref["energy"], rel=1e-8)
+    assert e == pytest.approx(plain["energy"], rel=1e-8)
+    assert _rel(x, ref["x"]) <= 1e-8
+
+
+def test_precond_switching_and_launch_path(bp):
+    """N = 40,000 (multi-launch MGS, symmetric kernel): precond and plain solves alternated in one
+    context (graph replay on in the GPU session: the per-step graphs are keyed by the mode) equal
+    fresh-context solves; the preconditioned solve needs fewer than half the iterations."""
+    p = _ragged(6, 20.0, 40000, 17, g.charges_in_ball(40, 15.0, 9))
+    res = {}
+    ctx = _ctx(bp, p)
+    assert ctx.arnoldi == 0
+    bp.bipb_source(ctx)
+    for mode in (0, 1, 0, 1):
+        ctx.set_precond(mode)
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 500, check_true=True)
+        assert st == bp.OK and rep["rel_res_true"] <= 1e-9
+        res.setdefault(mode, []).append((x, rep["iterations"], bp.bipb_energy(ctx, x)))
+    ctx.close()
+    for mode in (0, 1):
+        (xa, ia, ea), (xb, ib, eb) = res[mode]
+        assert ia == ib and np.array_equal(xa, xb) and ea == eb
+    assert res[1][0][1] * 2 < res[0][0][1]
+    assert res[1][0][2] == pytest.approx(res[0][0][2], rel=1e-8)
+
+
+def test_precond_batched_gmres(bp):
+    """The lockstep multi-RHS GMRES with the preconditioner equals the preconditioned single solves."""
+    p = g.sphere_problem(4, 4.0, g.charges_in_ball(20, 3.0, 2))
+    sets = [g.charges_in_ball(20, 3.0, s) for s in (2, 5)] + [g.helix_charges()]
+    ctx = _ctx(bp, p)
+    ctx.set_precond(1)
+    Bs, singles = [], []
+    for ch in sets:
+        bp.bipb_set_charges(ctx, ch)
+        Bs.append(bp.bipb_source(ctx))
+        x = np.zeros(2 * p.n)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 300)
+        singles.append((x, rep["iterations"]))
+    X = np.zeros((len(sets), 2 * p.n))
+    st, reps = bp.bipb_gmres_solve_batch(ctx, np.stack(Bs), X, 20, 1e-10, 300, check_true=True)
+    ctx.close()
+    assert st == bp.OK
+    for r in range(len(sets)):
+        assert abs(reps[r]["iterations"] - singles[r][1]) <= 1
+        assert reps[r]["rel_res_true"] <= 1e-9
+        assert _rel(X[r], singles[r][0]) <= 1e-9
+
+
+def test_precond_argument_errors(bp):
+    p = g.sphere_problem(2, 4.0, g.helix_charges())
+    ctx = _ctx(bp, p)
+    with pytest.raises(bp.BipbError) as ei:
+        ctx.set_precond(2)
+    assert ei.value.status == bp.ERR_ARG
+    assert ctx.precond == 0
+    ctx.close()

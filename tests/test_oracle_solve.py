@@ -137,3 +137,52 @@ def test_table2_trend_helix():
     assert es[0] < es[1] < es[2] < exact < 0
     paper = GOLD["table2_sphere"]["E_sol"]
     assert all(a < b for a, b in zip(paper, paper[1:]))  # same monotone approach in the paper
+
+
+# ---- right-preconditioned GMRES (jump-term diagonal; the library's opt-in bipb_set_precond) ----
+
+@pytest.mark.parametrize("m", [10, 20])
+def test_gmres_jacobi_vs_lapack_and_scaled_matrix(m):
+    """Right preconditioning M = diag(1/2 (1 + eps), 1/2 (1 + 1/eps)) (Saad Alg. 9.5): the solution is
+    LAPACK's; the iteration is plain GMRES on the explicitly scaled matrix A M^-1 (a different loop:
+    dense scaled matrix, plain core, x = M^-1 y), same iteration count; the estimate stays monotone
+    per cycle, the true residual meets the tolerance."""
+    p = g.sphere_problem(2, 4.0, g.helix_charges())
+    A = oracle.dense_assemble(p)
+    b = oracle.source(p)
+    eps = p.eps2 / p.eps1
+    minv = np.concatenate([np.full(p.n, 1.0 / (0.5 * (1 + eps))), np.full(p.n, 1.0 / (0.5 * (1 + 1 / eps)))])
+    x_lu = np.linalg.solve(A, b)
+    x, st, rep = oracle.gmres(p, b, restart=m, tol=1e-12, precond=True)
+    assert st == 0 and rep["rel_res_true"] < 1e-11
+    assert np.linalg.norm(x - x_lu) / np.linalg.norm(x_lu) < 1e-9
+    y, st2, rep2 = oracle.gmres_dense(A * minv[None, :], b, restart=m, tol=1e-12)
+    assert st2 == 0 and rep2["iterations"] == rep["iterations"]
+    assert np.linalg.norm(minv * y - x) / np.linalg.norm(x) < 1e-10
+    xd, _, rep3 = oracle.gmres_dense(A, b, restart=m, tol=1e-12, minv=minv)
+    assert rep3["iterations"] == rep["iterations"] and np.linalg.norm(xd - x) / np.linalg.norm(x) < 1e-10
+    h = rep["history"]
+    for c0 in range(0, len(h), m):
+        seg = h[c0:c0 + m]
+        assert np.all(np.diff(seg) <= 1e-15 * seg[0])
+
+
+def test_gmres_jacobi_identity_when_eps_is_one():
+    """eps1 = eps2 => M = I: the preconditioned iteration is the plain one, bit for bit."""
+    p = g.sphere_problem(2, 4.0, g.helix_charges(), eps2=1.0)
+    b = oracle.source(p)
+    x0, _, r0 = oracle.gmres(p, b, restart=10, tol=1e-12)
+    x1, _, r1 = oracle.gmres(p, b, restart=10, tol=1e-12, precond=True)
+    assert r0["iterations"] == r1["iterations"]
+    assert np.array_equal(x0, x1) and np.array_equal(r0["history"], r1["history"])
+
+
+def test_gmres_jacobi_same_energy_fewer_iterations():
+    """Same linear system => same solvation energy; the scaling of the 2x2 jump structure
+    (1/2 (1 + eps) = 40.5 vs 1/2 (1 + 1/eps) = 0.506) cuts the iteration count (L3: 27 -> 10)."""
+    p = g.sphere_problem(3, 4.0, g.charges_in_ball(20, 3.0, 7))
+    a = oracle.solve(p, restart=20, tol=1e-10)
+    j = oracle.solve(p, restart=20, tol=1e-10, precond=True)
+    assert j["report"]["rel_res_true"] <= 1e-9
+    assert j["energy"] == pytest.approx(a["energy"], rel=1e-8)
+    assert j["report"]["iterations"] <= 0.6 * a["report"]["iterations"]
