@@ -37,6 +37,8 @@ def test_native_arm_json():
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["cpu_baseline"]["kind"] == "oracle"
+    pc = d["precond"]  # the opt-in preconditioned solve, beside the headline
+    assert pc["energy_rel_diff_vs_plain"] <= 1e-8 and max(pc["iterations"]) < min(d["iterations"])
 
 
 @pytest.mark.gpu
