@@ -42,8 +42,12 @@ def _run(rank, world, uid, kind, exchange, q, size="big"):
         st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 300)
         phi = np.zeros(p.nc)
         e = bp.bipb_energy(ctx, x, phi)
+        ctx.set_precond(1)  # the opt-in preconditioned solve (replicated like the plain one)
+        xp = np.zeros(2 * p.n)
+        st, repp = bp.bipb_gmres_solve(ctx, xp, None, 20, 1e-10, 300)
         ctx.close()
-        q.put((rank, {"y": y, "Y": Y, "b": b, "x": x, "its": rep["iterations"], "e": e, "phi": phi}, None))
+        q.put((rank, {"y": y, "Y": Y, "b": b, "x": x, "its": rep["iterations"], "e": e, "phi": phi, "xp": xp,
+                      "its_p": repp["iterations"]}, None))
     except Exception as ex:  # pragma: no cover
         q.put((rank, None, repr(ex)))
 
@@ -77,7 +81,9 @@ def test_multirank_matches_single(world, kind, exchange):
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
     for o in outs:  # every rank holds the full, identical result
         assert np.array_equal(o["x"], outs[0]["x"]) and o["e"] == outs[0]["e"]
-        assert o["its"] == ref["its"]
+        assert o["its"] == ref["its"] and o["its_p"] == ref["its_p"] < ref["its"]
+        assert np.array_equal(o["xp"], outs[0]["xp"])
+        assert rel(o["xp"], ref["xp"]) <= (0.0 if kind == 0 else 1e-11)
         if kind == 0:
             assert np.array_equal(o["y"], ref["y"]) and np.array_equal(o["b"], ref["b"])
             assert np.array_equal(o["x"], ref["x"]) and o["e"] == ref["e"]
