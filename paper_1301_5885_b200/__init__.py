@@ -346,13 +346,22 @@ def bipb_destroy(ctx: Context):
     ctx.close()
 
 
-def solve(ctx: Context, x=None, restart_m=20, tol=1e-10, max_iters=500, check_true=False):
-    """Table 1 pipeline on the device: source -> GMRES -> energy.  Returns dict."""
-    b = bipb_source(ctx, None if x is None or isinstance(x, np.ndarray) else _zeros_like(x))
-    if x is None:
-        x = np.zeros(2 * ctx.n)
-    st, rep = bipb_gmres_solve(ctx, x, None, restart_m, tol, max_iters, check_true)
-    e = bipb_energy(ctx, x)
+def solve(ctx: Context, x=None, restart_m=20, tol=1e-10, max_iters=500, check_true=False, precond=None):
+    """Table 1 pipeline on the device: source -> GMRES -> energy.  Returns dict.
+    precond: None keeps the context's setting; 0 plain GMRES (the paper), 1 the opt-in right
+    jump-term diagonal preconditioner (bipb_set_precond) for this call only."""
+    prev = ctx.precond
+    if precond is not None:
+        ctx.set_precond(precond)
+    try:
+        b = bipb_source(ctx, None if x is None or isinstance(x, np.ndarray) else _zeros_like(x))
+        if x is None:
+            x = np.zeros(2 * ctx.n)
+        st, rep = bipb_gmres_solve(ctx, x, None, restart_m, tol, max_iters, check_true)
+        e = bipb_energy(ctx, x)
+    finally:
+        if precond is not None:
+            ctx.set_precond(prev)
     return {"b": b, "x": x, "status": st, "report": rep, "energy": e}
 
 
