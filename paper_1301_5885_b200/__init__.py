@@ -76,7 +76,7 @@ _SIGS = {
     "bipb_get_matvec_kernel": ([_P], _I32),
     "bipb_get_exchange": ([_P], _I32),
     "bipb_get_arnoldi": ([_P], _I32),
-    "bipb_set_precond": ([_P, _I32], _I32),
+    "bipb_set_precond": ([_P, _I32], ctypes.c_int),
     "bipb_get_precond": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
