@@ -1,5 +1,6 @@
 """Small end-to-end run for compute-sanitizer: row + symmetric (R = 1, 2, 4) matvecs, source,
-GMRES, energy, kappa > 0 and kappa = 0, ragged sizes."""
+GMRES (plain and preconditioned; fused cluster Arnoldi step), energy, kappa > 0 and kappa = 0,
+ragged sizes."""
 import os
 import sys
 
@@ -23,5 +24,6 @@ for kappa in (g.KAPPA, 0.0):
             bp.bipb_matvec(ctx, u)
             bp.bipb_matvec_batch(ctx, np.stack([u, 2 * u, 3 * u, u, u]))
             sol = bp.solve(ctx, restart_m=10, tol=1e-8)
+            sol = bp.solve(ctx, restart_m=10, tol=1e-8, precond=1)
         ctx.close()
 print("sanitize driver done")
