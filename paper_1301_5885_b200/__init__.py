@@ -78,6 +78,8 @@ _SIGS = {
     "bipb_get_arnoldi": ([_P], _I32),
     "bipb_set_precond": ([_P, _I32], ctypes.c_int),
     "bipb_get_precond": ([_P], _I32),
+    "bipb_set_sum_mode": ([_P, _I32], ctypes.c_int),
+    "bipb_get_sum_mode": ([_P], _I32),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_a, _r) in _SIGS.items():
@@ -175,6 +177,14 @@ class Context:
     @property
     def precond(self) -> int:
         return int(_lib.bipb_get_precond(self.handle))
+
+    # partial-sum mode of the symmetric product: 0 fixed-order doubles, 1 exact limbs (bipb.h) ----
+    def set_sum_mode(self, mode: int):
+        _check(_lib.bipb_set_sum_mode(self.handle, int(mode)))
+
+    @property
+    def sum_mode(self) -> int:
+        return int(_lib.bipb_get_sum_mode(self.handle))
 
     @property
     def arnoldi(self) -> int:
@@ -335,6 +345,15 @@ def bipb_set_precond(ctx: Context, kind: int):
 
 def bipb_get_precond(ctx: Context) -> int:
     return ctx.precond
+
+
+def bipb_set_sum_mode(ctx: Context, mode: int):
+    """0 = fixed-order double partials (default), 1 = exact fixed-point sums (bipb.h)."""
+    ctx.set_sum_mode(mode)
+
+
+def bipb_get_sum_mode(ctx: Context) -> int:
+    return ctx.sum_mode
 
 
 def bipb_get_arnoldi(ctx: Context) -> int:

@@ -2,6 +2,7 @@
 plain C-ABI shared object (include/bipb.h)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -9,8 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", f) for f in ("bipb.cu",)]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("bipb_kernels.cuh", "bipb_vec.cuh")] + [
-    os.path.join(ROOT, "include", "bipb.h")]
+DEPS = SRC + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "bipb.h")]
 LIB = os.path.join(HERE, "libbipb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -196,6 +196,14 @@ struct bipb_ctx {
     double *rec = nullptr, *fwd = nullptr, *rev = nullptr;
   } sym[3];
   double* sym_P = nullptr;  // [4][2][n] running row sums
+  // exact sums of the single-operand symmetric product (bipb_exact.cuh; bipb_set_sum_mode)
+  int sum_mode = 0;                   // 0 fixed-order double partials, 1 exact fixed-point limbs
+  bool exact_off = false;             // set after an out-of-range partial: double partials from then on
+  unsigned long long* xl = nullptr;   // [3][2n] row limbs + overflow count
+  int* xexp = nullptr;                // operand exponent max
+  int* xsticky = nullptr;             // set by finish_exact_kernel when a product overflowed
+  int xbias = 0;                      // BIPB_EXACT_BIAS test hook
+  double* x0save = nullptr;           // GMRES x0 kept for the double-partial rerun
   double* bat_U = nullptr;  // [4][2n] batch staging (host inputs)
   double* bat_Y = nullptr;
   int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
@@ -428,31 +436,73 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   const size_t rec_doubles = (size_t)cdiv(n, TILE) * TILE * F;  // tile-SoA, padded to whole tiles
   CK(dmalloc(c, &p.rec, rec_doubles * sizeof(double)));
   CK(cudaMemsetAsync(p.rec, 0, rec_doubles * sizeof(double), c->stream));
-  CK(dmalloc(c, &p.fwd, (size_t)p.group * p.runs * R * 2 * B * sizeof(double)));
-  CK(dmalloc(c, &p.rev, (size_t)p.group * (p.hmax + 1) * R * 2 * B * sizeof(double)));
   if (!c->sym_P) CK(dmalloc(c, &c->sym_P, (size_t)4 * 2 * n * sizeof(double)));
   p.R = R;
   return BIPB_OK;
 }
 
-// Y[r] = A U[r] for r < R (device, [R][2n] each; Y must not alias U)
+// the double partials of a plan, allocated on the first fixed-order product (exact sums need none)
+static bipb_status sym_partials(bipb_ctx* c, bipb_ctx::SymPlan* p, int R) {
+  if (p->fwd) return BIPB_OK;
+  CK(dmalloc(c, &p->fwd, (size_t)p->group * p->runs * R * 2 * p->B * sizeof(double)));
+  CK(dmalloc(c, &p->rev, (size_t)p->group * (p->hmax + 1) * R * 2 * p->B * sizeof(double)));
+  return BIPB_OK;
+}
+
+static bool exact_active(const bipb_ctx* c) { return c->sum_mode == 1 && !c->exact_off && c->mv_kind == 1; }
+
+// did an exact product since the last check have an out-of-range partial?  (the flag is derived
+// from the exchanged limbs, so every rank sees the same answer)  Switches the context to double
+// partials when it did.
+static bipb_status exact_overflowed(bipb_ctx* c, bool* out) {
+  *out = false;
+  if (!c->xsticky) return BIPB_OK;
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, c->xsticky, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h) {
+    CK(cudaMemsetAsync(c->xsticky, 0, sizeof(int), c->stream));
+    c->exact_off = true;
+    *out = true;
+  }
+  return BIPB_OK;
+}
+
+// Y[r] = A U[r] for r < R (device, [R][2n] each; Y must not alias U).  exact: R = 1 with exact
+// sums (bipb_exact.cuh) when the context asks for them.
 template <int R>
-static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
+static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y, bool allow_exact = false) {
   using Cfg = SymCfg<R>;
   const int64_t n = c->n;
   bipb_ctx::SymPlan* p;
   CKS(sym_plan<R>(c, &p));
-  LAUNCH1D(prescale_sym_kernel<R>, n, U, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, p->rec, n, c->s);
+  const bool exact = R == 1 && allow_exact && exact_active(c);
+  const int64_t xwords = 6 * n + 1;
+  if (exact) {
+    if (!c->xl) {
+      CK(dmalloc(c, &c->xl, (size_t)xwords * sizeof(unsigned long long)));
+      CK(dmalloc(c, &c->xexp, sizeof(int)));
+      CK(dmalloc(c, &c->xsticky, sizeof(int)));
+      CK(cudaMemsetAsync(c->xsticky, 0, sizeof(int), c->stream));
+    }
+    CK(cudaMemsetAsync(c->xl, 0, (size_t)xwords * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->xexp, 0, sizeof(int), c->stream));
+  } else {
+    CKS(sym_partials(c, p, R));
+  }
+  LAUNCH1D(prescale_sym_kernel<R>, n, U, c->ew, c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, p->rec, n, c->s,
+           exact ? c->xexp : nullptr);
   SymArgs a{};
   a.rec = p->rec; a.n = n; a.nb = p->nb; a.B = p->B; a.runs = p->runs; a.W = p->W; a.hmax = p->hmax;
   a.eps = c->eps; a.inveps = 1.0 / c->eps;
   a.sc1 = c->s; a.sc2 = c->s * c->s;
   a.fwd = p->fwd; a.rev = p->rev;
+  a.xl = exact ? c->xl : nullptr; a.xexp = c->xexp; a.xbias = c->xbias;
   const size_t smem =
       sizeof(double) * (STAGES * TILE * SymLayout<R>::F + (Cfg::TPB / 32) * R * 2 * sym_rs_rows(R, (int)p->B)) +
       8 * STAGES;
   const PeerBoxes nobox{};
-  if (p->I1 <= p->I0) {  // no I-blocks on this rank: its partial sums are zero
+  if (p->I1 <= p->I0 && !exact) {  // no I-blocks on this rank: its partial sums are zero
     if (c->p2p) {
       LAUNCH1D(reduce_sym_kernel<R>, n, p->fwd, p->rev, n, p->nb, p->B, p->runs, p->hmax, p->I0, p->I0, 1, c->sym_P,
                c->boxes, c->world, c->rank, c->p2p_stride, c->p2p_epoch);
@@ -460,8 +510,10 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
       CK(cudaMemsetAsync(c->sym_P, 0, (size_t)R * 2 * n * sizeof(double), c->stream));
     }
   }
-  for (int64_t Ia = p->I0; Ia < p->I1; Ia += p->group) {
-    const int64_t Ib = std::min(Ia + p->group, p->I1);
+  // exact sums need no partial memory: one launch unless BIPB_SYM_MEM_GB asks for groups (tests)
+  const int64_t group = (exact && !getenv("BIPB_SYM_MEM_GB")) ? std::max<int64_t>(1, p->I1 - p->I0) : p->group;
+  for (int64_t Ia = p->I0; Ia < p->I1; Ia += group) {
+    const int64_t Ib = std::min(Ia + group, p->I1);
     a.I0 = Ia;
     const int64_t grid = (Ib - Ia) * p->runs;
     if (grid > 2147483647LL) return fail(BIPB_ERR_ARG, "symmetric grid too large");
@@ -471,7 +523,10 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
     if constexpr (R == 1) {
       if (p->B == SymCfgMid::TPB * SymCfgMid::T) {
         using M = SymCfgMid;
-        auto k = c->screened ? sym_kernel<M::TPB, M::T, true, M::MINB, R> : sym_kernel<M::TPB, M::T, false, M::MINB, R>;
+        auto k = c->screened ? (exact ? sym_kernel<M::TPB, M::T, true, M::MINB, R, R == 1>
+                                      : sym_kernel<M::TPB, M::T, true, M::MINB, R>)
+                             : (exact ? sym_kernel<M::TPB, M::T, false, M::MINB, R, R == 1>
+                                      : sym_kernel<M::TPB, M::T, false, M::MINB, R>);
         CKS(set_smem(k, smem));
         k<<<(unsigned)grid, M::TPB, smem, c->stream>>>(a);
         mid = true;
@@ -479,16 +534,17 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
     }
     if (mid) {
     } else if (c->screened) {
-      auto k = sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R>;
+      auto k = exact ? sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R, R == 1> : sym_kernel<Cfg::TPB, Cfg::T, true, Cfg::MINB, R>;
       CKS(set_smem(k, smem));
       k<<<(unsigned)grid, Cfg::TPB, smem, c->stream>>>(a);
     } else {
-      auto k = sym_kernel<Cfg::TPB, Cfg::T, false, Cfg::MINB, R>;
+      auto k = exact ? sym_kernel<Cfg::TPB, Cfg::T, false, Cfg::MINB, R, R == 1> : sym_kernel<Cfg::TPB, Cfg::T, false, Cfg::MINB, R>;
       CKS(set_smem(k, smem));
       k<<<(unsigned)grid, Cfg::TPB, smem, c->stream>>>(a);
     }
     CK(cudaGetLastError());
     if (stop) CK(cudaEventRecord(stop, c->stream));
+    if (exact) continue;
     // the last group's epilogue stores the rank's row sums straight into every rank's mailbox
     const bool to_peers = c->p2p && Ib == p->I1;
     LAUNCH1D(reduce_sym_kernel<R>, n, p->fwd, p->rev, n, p->nb, p->B, p->runs, p->hmax, Ia, Ib, Ia == p->I0 ? 1 : 0,
@@ -496,6 +552,25 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
              c->p2p_epoch);
   }
   const double d1 = 0.5 * (1.0 + c->eps), d2 = 0.5 * (1.0 + 1.0 / c->eps);
+  if (exact) {
+    if (c->p2p) {  // limbs into slot [rank] of every mailbox, then the integer sum over the slots
+      LAUNCH1D(exact_publish_p2p_kernel, xwords, c->xl, xwords, c->boxes, c->world, c->rank, c->p2p_stride,
+               c->p2p_epoch);
+      CKS(p2p_publish_and_wait(c));
+      LAUNCH1D(finish_exact_kernel, 2 * n, reinterpret_cast<const unsigned long long*>(c->p2p_box), c->p2p_stride,
+               c->p2p_epoch, c->world, xwords, c->xexp, c->xbias, U, n, d1, d2, Y, c->xsticky);
+    } else {
+      if (c->sharded && !c->no_comm) {  // integer sums: exact in any reduction order
+        NcclApi& api = nccl();
+        ncclResult_t r = api.AllReduce(c->xl, c->xl, (size_t)xwords, ncclUint64, ncclSum, c->comm, c->stream);
+        if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+      }
+      LAUNCH1D(finish_exact_kernel, 2 * n, c->xl, 0, nullptr, 1, xwords, c->xexp, c->xbias, U, n, d1, d2, Y,
+               c->xsticky);
+    }
+    c->matvec_calls += 1;
+    return BIPB_OK;
+  }
   if (c->p2p) {
     CKS(p2p_publish_and_wait(c));
     LAUNCH1D(finish_sym_p2p_kernel<R>, n, c->p2p_box, c->p2p_stride, c->p2p_epoch, c->world, U, n, d1, d2, Y);
@@ -513,7 +588,7 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y) {
   return BIPB_OK;
 }
 
-static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) { return matvec_sym_R<1>(c, u, y); }
+static bipb_status matvec_sym_dev(bipb_ctx* c, const double* u, double* y) { return matvec_sym_R<1>(c, u, y, true); }
 
 // y = A u (device vectors of length 2n; y must not alias u)
 static bipb_status matvec_dev_impl(bipb_ctx* c, const double* u, double* y);
@@ -634,7 +709,7 @@ void bipb_destroy(bipb_ctx* c) {
   double* bufs[] = {c->ex, c->ey, c->ez, c->enx, c->eny, c->enz, c->ew, c->rec_el, c->qx, c->qy, c->qz, c->q4,
                     c->rec_ch, c->part, c->b, c->stage, c->gather, c->ubuf, c->ybuf, c->xbuf, c->bbuf, c->tbuf,
                     c->phit, c->phi, c->V, c->H, c->cs, c->sn, c->g, c->yk, c->scal, c->red_part,
-                    c->sym_P, c->bat_U, c->bat_Y, c->zbuf};
+                    c->sym_P, c->bat_U, c->bat_Y, c->zbuf, c->x0save};
   for (double* p : bufs)
     if (p) dfree(c, p);
   for (auto& sp : c->sym) {
@@ -644,6 +719,9 @@ void bipb_destroy(bipb_ctx* c) {
   }
   if (c->red_cnt) dfree(c, c->red_cnt);
   if (c->dflag) dfree(c, c->dflag);
+  if (c->xl) dfree(c, c->xl);
+  if (c->xexp) dfree(c, c->xexp);
+  if (c->xsticky) dfree(c, c->xsticky);
   if (c->p2p_epoch) dfree(c, c->p2p_epoch);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
@@ -847,6 +925,8 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->pinv1 = 1.0 / (0.5 * (1.0 + c->eps));  // opt-in right preconditioner M^-1 (bipb_set_precond)
   c->pinv2 = 1.0 / (0.5 * (1.0 + 1.0 / c->eps));
   if (const char* pe = getenv("BIPB_PRECOND")) c->precond = (!strcmp(pe, "jacobi") || !strcmp(pe, "1")) ? 1 : 0;
+  if (const char* se = getenv("BIPB_SUM")) c->sum_mode = (!strcmp(se, "exact") || !strcmp(se, "1")) ? 1 : 0;
+  if (const char* xb = getenv("BIPB_EXACT_BIAS")) c->xbias = atoi(xb);
   c->screened = kappa > 0.0;
   c->s = c->screened ? kappa : 1.0;
   c->rank = dist ? dist->rank : 0;
@@ -1033,7 +1113,11 @@ bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
   CKS(vec_where(c, y, &ydev));
   double* yd = ydev ? y : c->ybuf;
   if (ydev && yd == ud) return fail(BIPB_ERR_ARG, "u and y must not alias");
+  const bool exact = exact_active(c);
   CKS(matvec_dev(c, ud, yd));
+  bool ovf = false;
+  if (exact) CKS(exact_overflowed(c, &ovf));
+  if (ovf) CKS(matvec_dev(c, ud, yd));  // out-of-range partial: the fixed-order double partials
   if (!ydev) CK(cudaMemcpyAsync(y, yd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return BIPB_OK;
@@ -1386,6 +1470,17 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
   bool converged = false;
   double rel = 1.0, h2[2];
   if (rep) rep->rel_res_true = -1.0;
+  // exact sums: an out-of-range partial (NaN product, bipb_exact.cuh) restarts the solve from x0
+  // with the fixed-order double partials
+  const bool exact = exact_active(c);
+  if (exact) {
+    if (!c->x0save) CK(dmalloc(c, &c->x0save, m2 * sizeof(double)));
+    CK(cudaMemcpyAsync(c->x0save, xd, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+rerun:
+  its = restarts = matvecs = hl = 0;
+  converged = false;
+  rel = 1.0;
 
   CKS(dot_dev(c, bd, bd, m2, 1.0, S + 0));
   LAUNCH1D(sqrt_kernel, 1, S + 0, S + 0);
@@ -1432,6 +1527,7 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
         kdone = k + 1;
         if (hk1 <= 1e-14 * beta_b) break;  // happy breakdown
         if (rel <= tol || its >= max_iters) break;
+        if (exact && !(rel == rel)) break;
       }
       backsolve_kernel<<<1, 1, 0, c->stream>>>(c->H, c->g, c->yk, kdone, m);
       c->launches_all++;
@@ -1441,6 +1537,7 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
         LAUNCH1D(update_x_kernel, m2, xd, c->V, c->yk, kdone, m2);
       if (rel <= tol) { converged = true; break; }
       if (its >= max_iters) break;
+      if (exact && !(rel == rel)) break;
     }
     if (check_true) {
       CKS(matvec_dev(c, xd, c->tbuf));
@@ -1450,6 +1547,14 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
       LAUNCH1D(sqrt_kernel, 1, S + 4, S + 4);
       CKS(read_scalars(c, S + 4, 1, h2));
       if (rep) rep->rel_res_true = h2[0] / beta_b;
+    }
+  }
+  if (exact && c->sum_mode == 1 && !c->exact_off) {
+    bool ovf = false;
+    CKS(exact_overflowed(c, &ovf));
+    if (ovf) {
+      CK(cudaMemcpyAsync(xd, c->x0save, m2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      goto rerun;
     }
   }
   if (!xdev) CK(cudaMemcpyAsync(x, xd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1621,6 +1726,18 @@ bipb_status bipb_set_precond(bipb_ctx* c, int32_t kind) {
   return BIPB_OK;
 }
 int32_t bipb_get_precond(bipb_ctx* c) { return c ? c->precond : -1; }
+
+bipb_status bipb_set_sum_mode(bipb_ctx* c, int32_t mode) {
+  if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  if (mode != 0 && mode != 1) return fail(BIPB_ERR_ARG, "sum mode must be 0 (fixed-order doubles) or 1 (exact)");
+  c->sum_mode = mode;
+  c->exact_off = false;
+  return BIPB_OK;
+}
+int32_t bipb_get_sum_mode(bipb_ctx* c) {
+  if (!c) return -1;
+  return exact_active(c) ? 1 : 0;
+}
 
 int32_t bipb_get_exchange(bipb_ctx* c) {
   if (!c) return -1;

@@ -22,6 +22,7 @@
 #pragma once
 #include "bipb_kernels.cuh"
 #include "bipb_p2p.cuh"
+#include "bipb_exact.cuh"
 
 namespace bipb {
 
@@ -65,6 +66,11 @@ struct SymArgs {
   double sc1, sc2;    // s, s^2
   double* fwd;        // [nI][runs][R][2][B]   forward sums of tile run (I, run), I - I0
   double* rev;        // [nI][hmax+1][R][2][B] reverse sums of tile (I, J = I+o), I - I0
+  // exact sums (bipb_exact.cuh; R = 1 only): when xl != nullptr every partial is added to the
+  // row limbs xl[3][2n] (+ overflow count) instead of being written to fwd / rev
+  unsigned long long* xl;
+  const int* xexp;    // largest exponent field of the operand weights (prescale_sym_kernel)
+  int xbias;          // test hook: added to the shift S (forces the out-of-range fallback)
 };
 
 // number of offsets (including the diagonal o = 0) for block I in the circulant schedule
@@ -158,8 +164,9 @@ __device__ __forceinline__ void pair_sym(const SymSrc<R>& ti, const SymSrc<R>& s
   }
 }
 
-template <int TPB, int T, bool SCREENED, int MINB, int R>
+template <int TPB, int T, bool SCREENED, int MINB, int R, bool EXACT = false>
 __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
+  static_assert(!EXACT || R == 1, "exact sums: single operand only");
   constexpr int NW = TPB / 32;
   constexpr int B = TPB * T;
   constexpr int F = SymLayout<R>::F;
@@ -402,14 +409,17 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
             q0 += rsum[((w * R + r) * 2) * RS + jt];
             q1 += rsum[((w * R + r) * 2 + 1) * RS + jt];
           }
-          double* rv0 = a.rev + (((Il * (a.hmax + 1) + o) * R + r) * 2) * B;
-          if constexpr (SCREENED) {
-            rv0[jl] = a.sc1 * q0;
-            rv0[B + jl] = a.sc2 * q1;
-          } else {
-            rv0[jl] = (a.eps - 1.0) * q0;
-            rv0[B + jl] = -((1.0 - a.inveps) * q1);
+          const double v0 = SCREENED ? a.sc1 * q0 : (a.eps - 1.0) * q0;
+          const double v1 = SCREENED ? a.sc2 * q1 : -((1.0 - a.inveps) * q1);
+          if constexpr (EXACT) {
+            const double p2s = exact_scale_dev(a.xexp, a.xbias);
+            exact_add(a.xl, 2 * a.n, J * B + jl, v0, p2s);
+            exact_add(a.xl, 2 * a.n, a.n + J * B + jl, v1, p2s);
+            continue;
           }
+          double* rv0 = a.rev + (((Il * (a.hmax + 1) + o) * R + r) * 2) * B;
+          rv0[jl] = v0;
+          rv0[B + jl] = v1;
         }
       }
       __syncthreads();  // rsum reused
@@ -422,14 +432,19 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
     const int l = threadIdx.x + k * TPB;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double* f0 = a.fwd + (((Il * a.runs + run) * R + r) * 2) * B;
-      if (SCREENED) {
-        f0[l] = a.sc1 * fa[k][r].p0;
-        f0[B + l] = a.sc2 * fa[k][r].p1;
-      } else {
-        f0[l] = (a.eps - 1.0) * fa[k][r].p0;
-        f0[B + l] = -((1.0 - a.inveps) * fa[k][r].p1);
+      const double v0 = SCREENED ? a.sc1 * fa[k][r].p0 : (a.eps - 1.0) * fa[k][r].p0;
+      const double v1 = SCREENED ? a.sc2 * fa[k][r].p1 : -((1.0 - a.inveps) * fa[k][r].p1);
+      if constexpr (EXACT) {
+        if (gi[k] < a.n) {
+          const double p2s = exact_scale_dev(a.xexp, a.xbias);
+          exact_add(a.xl, 2 * a.n, gi[k], v0, p2s);
+          exact_add(a.xl, 2 * a.n, a.n + gi[k], v1, p2s);
+        }
+        continue;
       }
+      double* f0 = a.fwd + (((Il * a.runs + run) * R + r) * 2) * B;
+      f0[l] = v0;
+      f0[B + l] = v1;
     }
   }
 }
@@ -440,8 +455,9 @@ __global__ void prescale_sym_kernel(const double* __restrict__ U, const double* 
                                     const double* __restrict__ ex, const double* __restrict__ ey,
                                     const double* __restrict__ ez, const double* __restrict__ nx,
                                     const double* __restrict__ ny, const double* __restrict__ nz,
-                                    double* __restrict__ rec, int64_t n, double s) {
+                                    double* __restrict__ rec, int64_t n, double s, int* __restrict__ xexp) {
   constexpr int F = SymLayout<R>::F;
+  int emax = 0;  // exact sums: largest exponent field of the weights c, a'
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     using L = SymLayout<R>;
     double* p = rec + sym_idx(j, 0, F);
@@ -453,10 +469,14 @@ __global__ void prescale_sym_kernel(const double* __restrict__ U, const double* 
     p[(L::NX + 2) * TILE] = nz[j];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      p[L::C(r) * TILE] = w[j] * U[(int64_t)r * 2 * n + n + j];
-      p[L::A(r) * TILE] = s * (w[j] * U[(int64_t)r * 2 * n + j]);
+      const double cw = w[j] * U[(int64_t)r * 2 * n + n + j];
+      const double aw = s * (w[j] * U[(int64_t)r * 2 * n + j]);
+      p[L::C(r) * TILE] = cw;
+      p[L::A(r) * TILE] = aw;
+      emax = max(emax, max(exact_exp_field(cw), exact_exp_field(aw)));
     }
   }
+  if (xexp) exact_note_exp(xexp, emax);
 }
 
 // Add one launch group's partials to the running row sums P = [R][2][n] (P0 | P1 blocks).

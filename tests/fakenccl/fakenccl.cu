@@ -48,6 +48,10 @@ __global__ void accumulate(double* dst, const double* src, size_t n, int first) 
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     dst[i] = first ? src[i] : dst[i] + src[i];
 }
+__global__ void accumulate_u64(unsigned long long* dst, const unsigned long long* src, size_t n, int first) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = first ? src[i] : dst[i] + src[i];
+}
 }  // namespace
 
 extern "C" {
@@ -100,12 +104,17 @@ ncclResult_t ncclAllGather(const void* send, void* recv, size_t count, ncclDataT
 ncclResult_t ncclAllReduce(const void* send, void* recv, size_t count, ncclDataType_t dt, ncclRedOp_t op,
                            ncclComm_t comm, cudaStream_t st) {
   Comm* c = (Comm*)comm;
-  if (dt != ncclFloat64 || op != ncclSum || count * 8 > CAP) return ncclInvalidArgument;
+  const bool u64 = dt == ncclUint64 || dt == ncclInt64;  // exact sums (bipb_exact.cuh)
+  if ((dt != ncclFloat64 && !u64) || op != ncclSum || count * 8 > CAP) return ncclInvalidArgument;
   cudaMemcpyAsync(c->mine, send, count * 8, cudaMemcpyDeviceToDevice, st);
   cudaStreamSynchronize(st);
   barrier(c);
   for (int p = 0; p < c->n; ++p)
-    accumulate<<<256, 256, 0, st>>>((double*)recv, (const double*)c->peer[p], count, p == 0);
+    if (u64)
+      accumulate_u64<<<256, 256, 0, st>>>((unsigned long long*)recv, (const unsigned long long*)c->peer[p], count,
+                                          p == 0);
+    else
+      accumulate<<<256, 256, 0, st>>>((double*)recv, (const double*)c->peer[p], count, p == 0);
   cudaStreamSynchronize(st);
   barrier(c);
   return ncclSuccess;

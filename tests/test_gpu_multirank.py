@@ -23,8 +23,9 @@ def _problem(size="big"):
     return g.sphere_problem(5, 4.0, g.charges_in_ball(30, 3.0, 17))  # N = 20480 (symmetric default)
 
 
-def _run(rank, world, uid, kind, exchange, q, size="big"):
+def _run(rank, world, uid, kind, exchange, q, size="big", sum_mode="fixed"):
     os.environ["BIPB_NCCL_LIB"] = FAKE
+    os.environ["BIPB_SUM"] = sum_mode  # exact: integer limb sums (bipb_exact.cuh)
     os.environ["BIPB_GRAPHS"] = "0"  # the stand-in synchronises inside collectives: not capturable
     os.environ["BIPB_EXCHANGE"] = exchange  # nccl: collectives; p2p: peer stores (bipb_p2p.cuh)
     try:
@@ -33,6 +34,7 @@ def _run(rank, world, uid, kind, exchange, q, size="big"):
         dist = None if world == 0 else (rank, world, uid, 0)
         ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
         ctx.set_matvec_kernel(kind)
+        assert ctx.sum_mode == (1 if sum_mode == "exact" and kind == 1 else 0)
         assert ctx.exchange == ("none" if world == 0 else exchange)
         u = g.random_vector(2 * p.n, 5)
         y = bp.bipb_matvec(ctx, u)
@@ -52,7 +54,7 @@ def _run(rank, world, uid, kind, exchange, q, size="big"):
         q.put((rank, None, repr(ex)))
 
 
-def _spawn(world, kind, exchange="nccl", size="big"):
+def _spawn(world, kind, exchange="nccl", size="big", sum_mode="fixed"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     uid = None
@@ -60,7 +62,8 @@ def _spawn(world, kind, exchange="nccl", size="big"):
         # must not load the stand-in into its own copy of the library)
         import time
         uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
-    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, exchange, q, size)) for r in range(max(world, 1))]
+    procs = [ctx.Process(target=_run, args=(r, world, uid, kind, exchange, q, size, sum_mode))
+             for r in range(max(world, 1))]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -107,3 +110,17 @@ def test_multirank_tiny_problem(kind, exchange):
         np.testing.assert_allclose(o["x"], ref["x"], rtol=1e-11, atol=1e-13 * np.abs(ref["x"]).max())
         assert np.array_equal(o["b"], ref["b"])
         assert o["e"] == pytest.approx(ref["e"], rel=1e-12)
+
+
+@pytest.mark.parametrize("size", ["big", "tiny"])
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_multirank_exact_sums_bitwise(world, exchange, size):
+    """Exact limb sums (bipb_set_sum_mode 1): the symmetric product, the replicated GMRES and the
+    energy are bitwise the single-GPU results for every rank count and both exchanges."""
+    ref = _spawn(0, 1, size=size, sum_mode="exact")[0]
+    outs = _spawn(world, 1, exchange, size=size, sum_mode="exact")
+    for o in outs:
+        assert np.array_equal(o["y"], ref["y"]) and np.array_equal(o["x"], ref["x"])
+        assert o["its"] == ref["its"] and o["e"] == ref["e"]
+        assert np.array_equal(o["xp"], ref["xp"])
