@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--precond-steps", type=int, default=None,
                     help="extra steps with the opt-in GMRES preconditioner (reported under 'precond'; 0 = skip)")
+    ap.add_argument("--sum", default=None, choices=["fixed", "exact"],
+                    help="partial-sum mode of the symmetric product (bipb_set_sum_mode; default: the library's)")
     return ap.parse_args()
 
 
@@ -202,6 +204,8 @@ def run_native(args):
     cen, nrm, area, chg = T(prob.centroids), T(prob.normals), T(prob.areas), T(prob.charges)
     ctx = bp.bipb_setup(cen, nrm, area, chg, prob.eps1, prob.eps2, prob.kappa, dist=dist_arg,
                         stream=stream.cuda_stream)
+    if args.sum is not None:
+        ctx.set_sum_mode(1 if args.sum == "exact" else 0)
     x = torch.zeros(2 * n, dtype=torch.float64, device=dev)
     b = torch.zeros(2 * n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -254,6 +258,7 @@ def run_native(args):
     pairs_per_step = [mv * n * (n - 1) + 2 * n * nc for mv in matvecs]
     value = sum(pairs_per_step) / (total_ms / 1e3)
     kind = ctx.matvec_kernel
+    exact = ctx.sum_mode == 1  # still 1 after the run: no out-of-range fallback happened
     if kind == 1:  # symmetric: pairs evaluated by this rank = its I-blocks' share of all pairs
         pairs_per_launch = n * (n - 1) // world
     else:
@@ -265,12 +270,12 @@ def run_native(args):
     traffic = None
     try:
         tj = json.load(open(TRAFFIC_JSON))
-        traffic = tj.get(str(kind), {}).get("bytes_per_launch")
+        traffic = tj.get(str(kind) + ("x" if exact else ""), {}).get("bytes_per_launch")
     except Exception:
         pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": KERNEL_NAME[kind], "flops_per_unit": F_ALG,
+                "kernel": KERNEL_NAME[kind] + (" with exact limb sums" if exact else ""), "flops_per_unit": F_ALG,
                 "unit_of_work": "ordered matvec pair-interaction (i, j != i)",
                 "units_per_launch": pairs_per_launch, "avg_launch_ms": avg_launch_ms, "launches": mv_launches,
                 "launch_note": "one 'launch' = one operator application (all I-block groups of the symmetric kernel)",
@@ -285,7 +290,9 @@ def run_native(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges, bipb_inputs)",
-            "config": dict(bench_config(prob, world), exchange=ctx.exchange),
+            "config": dict(bench_config(prob, world), exchange=ctx.exchange,
+                           sums=("exact fixed-point limbs" if exact else "fixed-order double partials")
+                           if kind == 1 else "fixed-order chunk partials"),
             "time_to_solution_s": total_ms / args.steps / 1e3,
             "iterations": [r["iterations"] for r in reps], "matvecs": matvecs,
             "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),

@@ -197,7 +197,7 @@ struct bipb_ctx {
   } sym[3];
   double* sym_P = nullptr;  // [4][2][n] running row sums
   // exact sums of the single-operand symmetric product (bipb_exact.cuh; bipb_set_sum_mode)
-  int sum_mode = 0;                   // 0 fixed-order double partials, 1 exact fixed-point limbs
+  int sum_mode = 1;                   // 1 exact fixed-point limbs (default), 0 fixed-order double partials
   bool exact_off = false;             // set after an out-of-range partial: double partials from then on
   unsigned long long* xl = nullptr;   // [3][2n] row limbs + overflow count
   int* xexp = nullptr;                // operand exponent max
@@ -222,11 +222,11 @@ struct bipb_ctx {
   EventPool pool[3];
   int64_t launches_all = 0;
   int64_t matvec_calls = 0;  // operator applications (for per-product kernel time)
-  int warm_kind = -1;        // matvec kind whose buffers / attributes exist (eager product done)
+  int warm_kind = -1;        // 2 kind + exact sums: the product whose buffers / attributes exist (eager product done)
   // CUDA graphs of the GMRES Arnoldi steps (one per k), valid for (V, m, n, kind)
   struct {
     const double* V = nullptr;
-    int m = 0, kind = -1, precond = -1;
+    int m = 0, kind = -1, precond = -1, exact = -1;
     std::vector<cudaGraphExec_t> ex;
   } ag;
 };
@@ -450,6 +450,9 @@ static bipb_status sym_partials(bipb_ctx* c, bipb_ctx::SymPlan* p, int R) {
 }
 
 static bool exact_active(const bipb_ctx* c) { return c->sum_mode == 1 && !c->exact_off && c->mv_kind == 1; }
+// which product variant an eager call has prepared (buffers allocated, attributes set): graph
+// capture of the Arnoldi steps waits for it
+static int warm_key(const bipb_ctx* c) { return 2 * c->mv_kind + (exact_active(c) ? 1 : 0); }
 
 // did an exact product since the last check have an out-of-range partial?  (the flag is derived
 // from the exchanged limbs, so every rank sees the same answer)  Switches the context to double
@@ -596,7 +599,7 @@ static bipb_status matvec_dev(bipb_ctx* c, const double* u, double* y) {
   CKS(matvec_dev_impl(c, u, y));
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
-  if (cs == cudaStreamCaptureStatusNone) c->warm_kind = c->mv_kind;
+  if (cs == cudaStreamCaptureStatusNone) c->warm_kind = warm_key(c);
   return BIPB_OK;
 }
 static bipb_status matvec_dev_impl(bipb_ctx* c, const double* u, double* y) {
@@ -925,7 +928,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   c->pinv1 = 1.0 / (0.5 * (1.0 + c->eps));  // opt-in right preconditioner M^-1 (bipb_set_precond)
   c->pinv2 = 1.0 / (0.5 * (1.0 + 1.0 / c->eps));
   if (const char* pe = getenv("BIPB_PRECOND")) c->precond = (!strcmp(pe, "jacobi") || !strcmp(pe, "1")) ? 1 : 0;
-  if (const char* se = getenv("BIPB_SUM")) c->sum_mode = (!strcmp(se, "exact") || !strcmp(se, "1")) ? 1 : 0;
+  if (const char* se = getenv("BIPB_SUM")) c->sum_mode = (!strcmp(se, "fixed") || !strcmp(se, "0")) ? 0 : 1;
   if (const char* xb = getenv("BIPB_EXACT_BIAS")) c->xbias = atoi(xb);
   c->screened = kappa > 0.0;
   c->s = c->screened ? kappa : 1.0;
@@ -1220,9 +1223,11 @@ static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
   // opt-in (BIPB_GRAPHS=1): replay pays off only from the second solve in a context (measured:
   // C1 3.25 -> 2.82 ms per solve, C2 -2.6%, C3/C4 within noise; the first solve pays the capture)
   static const bool graphs_on = getenv("BIPB_GRAPHS") && !strcmp(getenv("BIPB_GRAPHS"), "1");
-  const bool use = graphs_on && !c->timing && c->warm_kind == c->mv_kind;
+  const bool use = graphs_on && !c->timing && c->warm_kind == warm_key(c);
   if (use) {
-    if (c->ag.V != c->V || c->ag.m != m || c->ag.kind != c->mv_kind || c->ag.precond != c->precond) {
+    const int exact = exact_active(c) ? 1 : 0;  // the captured product differs per sum mode
+    if (c->ag.V != c->V || c->ag.m != m || c->ag.kind != c->mv_kind || c->ag.precond != c->precond ||
+        c->ag.exact != exact) {
       for (auto e : c->ag.ex)
         if (e) cudaGraphExecDestroy(e);
       c->ag.ex.assign(m, nullptr);
@@ -1230,6 +1235,7 @@ static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
       c->ag.m = m;
       c->ag.kind = c->mv_kind;
       c->ag.precond = c->precond;
+      c->ag.exact = exact;
     }
     if (!c->ag.ex[k]) {
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
