@@ -426,9 +426,12 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   p.hmax = (p.nb & 1) ? (p.nb - 1) / 2 : p.nb / 2;
   bipb_partition(p.nb, c->world, c->rank, &p.I0, &p.I1);
   const int64_t tiles_local = (p.I1 - p.I0) * (p.hmax + 1);
-  // runs of W offsets per CTA: >= 16 waves of resident CTAs (2 per SM) on this rank, W <= 16
-  p.W = std::max<int64_t>(1, std::min<int64_t>(16, tiles_local / (148 * 2 * 16)));
-  p.runs = cdiv(p.hmax + 1, p.W);
+  // runs of W offsets per CTA: >= 32 waves of resident CTAs (2 per SM) on this rank, W <= 4 (short
+  // CTAs of nearly equal work keep the launch's tail small; measured at C4, profiles/r01/session3/
+  // sweepW_C4.jsonl: W = 16 192.7 ms, 8 192.8, 6 191.9, 4 191.7 per product)
+  p.W = std::max<int64_t>(1, std::min<int64_t>(4, tiles_local / (148 * 2 * 32)));
+  if (const char* e = getenv("BIPB_SYM_W")) p.W = std::max<int64_t>(1, atoll(e));  // tuning
+  p.runs = cdiv(p.hmax + 1, p.W);  // an I-block's offsets split evenly over its runs (bipb_sym.cuh)
   double gb = 4.0;
   if (const char* e = getenv("BIPB_SYM_MEM_GB")) gb = std::max(0.001, atof(e));
   const double per_block = (double)((p.hmax + 1) + p.runs) * R * 2 * B * sizeof(double);

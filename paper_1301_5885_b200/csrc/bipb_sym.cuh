@@ -188,8 +188,10 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
   const int64_t I = a.I0 + Il;
   const int64_t run = blockIdx.x % a.runs;
   const int64_t noff = sym_noff(I, a.nb);
-  const int64_t o0 = run * a.W;
-  const int64_t o1 = (o0 + a.W < noff) ? o0 + a.W : noff;
+  // the I-block's noff offsets split evenly over its runs (sizes differ by at most one, no tiny
+  // last run: the CTAs have nearly equal work, which shortens the launch's tail)
+  const int64_t o0 = run * noff / a.runs;
+  const int64_t o1 = (run + 1) * noff / a.runs;
   const int64_t i0 = I * B;
   constexpr int64_t stages_per_block = B / TILE;
 
