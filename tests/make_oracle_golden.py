@@ -17,11 +17,24 @@ import bipb_inputs as g  # noqa: E402
 import oracle  # noqa: E402
 
 
+def _host():
+    """CPU model and thread count the oracle ran on (recorded beside the golden values)."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+
 def main(names, restarts=(20,), outdir=None):
     for name in names:
         p = g.config(name)
         out = {"config": name, "sha256": p.sha256(), "n": p.n, "nc": p.nc, "eps1": p.eps1, "eps2": p.eps2,
-               "kappa": p.kappa, "tol": 1e-10, "solves": {}}
+               "kappa": p.kappa, "tol": 1e-10, "solves": {}, "host": _host()}
         rows = np.unique(np.linspace(0, p.n - 1, 64).astype(np.int64))
         for m in restarts:
             t = time.time()
