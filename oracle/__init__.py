@@ -58,6 +58,8 @@ def lib():
             ("orc_gmres_dense", [i, p, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
             ("orc_gmres_bem", [i, p, p, p, d, d, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
             ("orc_gmres_dense_prec", [i, p, p, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
+            ("orc_gmres_op", [i, ctypes.c_void_p, ctypes.c_void_p, p, p, i, d, i, i, ctypes.POINTER(Report)],
+             ctypes.c_int),
             ("orc_gmres_bem_jacobi", [i, p, p, p, d, d, p, p, i, d, i, i, ctypes.POINTER(Report)], ctypes.c_int),
             ("orc_reaction_potential", [i, p, p, p, d, d, i, p, p, p], None),
             ("orc_energy", [i, p, p, p, d, d, i, p, p, p], d),
@@ -189,6 +191,67 @@ def gmres(prob, b, x0=None, restart=20, tol=1e-10, max_iters=500, check_true=Tru
     st = fn(prob.n, _p(_c(prob.centroids)), _p(_c(prob.normals)), _p(_c(prob.areas)),
             eps_ratio(prob.eps1, prob.eps2), prob.kappa, _p(b), _p(x), restart, tol,
             max_iters, int(check_true), ctypes.byref(rep))
+    return x, st, _report(rep, hist)
+
+
+_OP_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, _D, _D)
+
+
+def gmres_checkpointed(prob, b, store, restart=20, tol=1e-10, max_iters=500, check_true=True, log=None):
+    """Plain GMRES exactly as `gmres` (the same gmres_core in oracle.c), with every operator
+    product y = A x computed by orc_matvec and kept in the directory `store` as
+    `<call index>_<sha256(x)[:16]>.npy`.  A rerun replays the stored products (bitwise the same
+    arithmetic: GMRES is deterministic, so the k-th call sees the same x) and computes only the
+    missing ones, so a full-size solve can be spread over several time-limited processes.  A stored
+    product whose input hash differs from the replayed x raises (the run diverged)."""
+    import hashlib
+    import time
+    os.makedirs(store, exist_ok=True)
+    m = 2 * prob.n
+    cen, nrm, area = _c(prob.centroids), _c(prob.normals), _c(prob.areas)
+    eps = eps_ratio(prob.eps1, prob.eps2)
+    have = {}
+    for f in os.listdir(store):
+        if f.endswith(".npy") and not f.startswith("."):
+            k, h = f[:-4].split("_", 1)
+            have[int(k)] = (h, os.path.join(store, f))
+    calls = [0]
+    err = []
+
+    def op(_ctx, xp, yp):
+        k = calls[0]
+        calls[0] += 1
+        if err:
+            return
+        xv = np.ctypeslib.as_array(xp, (m,))
+        yv = np.ctypeslib.as_array(yp, (m,))
+        h = hashlib.sha256(xv.tobytes()).hexdigest()[:16]
+        if k in have:
+            if have[k][0] != h:
+                err.append(f"stored product {k} was made from another x ({have[k][0]} vs {h})")
+                yv[:] = np.nan
+                return
+            yv[:] = np.load(have[k][1])
+            if log:
+                log(f"product {k}: replayed")
+            return
+        t = time.time()
+        lib().orc_matvec(prob.n, _p(cen), _p(nrm), _p(area), eps, prob.kappa, xp, yp)
+        tmp = os.path.join(store, f".{k}_{h}.npy")
+        np.save(tmp, np.array(yv))
+        os.replace(tmp, os.path.join(store, f"{k:03d}_{h}.npy"))
+        if log:
+            log(f"product {k}: computed in {time.time() - t:.1f} s")
+
+    cb = _OP_FN(op)
+    b = _c(b)
+    x = np.zeros(m)
+    hist = np.zeros(max_iters + 1)
+    rep = Report(history=_p(hist), history_cap=hist.size)
+    st = lib().orc_gmres_op(m, ctypes.cast(cb, ctypes.c_void_p), None, _p(b), _p(x), restart, tol, max_iters,
+                            int(check_true), ctypes.byref(rep))
+    if err:
+        raise RuntimeError(err[0])
     return x, st, _report(rep, hist)
 
 

@@ -352,6 +352,14 @@ int orc_gmres_bem(int64_t n, const double* cen, const double* nrm, const double*
   bem_ctx c = {n, cen, nrm, area, eps, kappa};
   return gmres_core(bem_op, &c, 2 * n, b, x, restart, tol, max_iters, check_true, NULL, rep);
 }
+/* The same GMRES (gmres_core, unchanged) with the operator supplied by the caller: a C callback
+ * op(ctx, x, y) that must set y = A x.  Used by oracle.gmres_checkpointed, whose callback is
+ * orc_matvec behind an on-disk store of the products (so a long full-size solve can be split
+ * across several processes and replays bitwise the same arithmetic). */
+int orc_gmres_op(int64_t m, orc_op_fn op, void* ctx, const double* b, double* x, int64_t restart, double tol,
+                 int64_t max_iters, int64_t check_true, orc_report* rep) {
+  return gmres_core(op, ctx, m, b, x, restart, tol, max_iters, check_true, NULL, rep);
+}
 /* GMRES on the BEM operator, right-preconditioned by the diagonal of the jump terms of
  * Eqs. (12)-(13): M = diag(1/2 (1 + eps) I_N, 1/2 (1 + 1/eps) I_N) (not in the paper; the
  * library's opt-in bipb_set_precond(ctx, 1)).  Same linear system, same residual test. */

@@ -1,6 +1,8 @@
 """Write tests/golden/oracle_<cfg>.json: full oracle solves (source -> GMRES -> energy) of
 BASELINE configs, keyed by the input SHA-256.  Calls ONLY oracle/ and bipb_inputs/
-(never the CUDA path).  Usage: python tests/make_oracle_golden.py C1 C2 [C3 ...]"""
+(never the CUDA path).  Usage: python tests/make_oracle_golden.py C1 C2 [C3 ...] [--out=DIR] [--store=DIR]
+(--store: GMRES products kept on disk, oracle.gmres_checkpointed; used for C4, whose solve takes
+longer than one GPU-box call, tools/c4_golden_box.sh)."""
 import json
 import os
 import sys
@@ -30,7 +32,7 @@ def _host():
     return {"cpu_model": model, "nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
 
 
-def main(names, restarts=(20,), outdir=None):
+def main(names, restarts=(20,), outdir=None, store=None):
     for name in names:
         p = g.config(name)
         out = {"config": name, "sha256": p.sha256(), "n": p.n, "nc": p.nc, "eps1": p.eps1, "eps2": p.eps2,
@@ -38,7 +40,14 @@ def main(names, restarts=(20,), outdir=None):
         rows = np.unique(np.linspace(0, p.n - 1, 64).astype(np.int64))
         for m in restarts:
             t = time.time()
-            r = oracle.solve(p, restart=m, tol=1e-10, max_iters=500, check_true=True)
+            if store:  # products kept on disk: the solve can span several time-limited runs
+                b = oracle.source(p)
+                x, st, rep = oracle.gmres_checkpointed(p, b, os.path.join(store, f"{name}_m{m}"), restart=m,
+                                                       tol=1e-10, max_iters=500, check_true=True,
+                                                       log=lambda s: print(name, s, flush=True))
+                r = {"b": b, "x": x, "status": st, "report": rep, "energy": oracle.energy(p, x)}
+            else:
+                r = oracle.solve(p, restart=m, tol=1e-10, max_iters=500, check_true=True)
             out["solves"][str(m)] = {
                 "energy": r["energy"], "status": r["status"], "iterations": r["report"]["iterations"],
                 "restarts": r["report"]["restarts"], "matvecs": r["report"]["matvecs"],
@@ -53,7 +62,7 @@ def main(names, restarts=(20,), outdir=None):
 
 
 if __name__ == "__main__":
-    args = [a for a in sys.argv[1:] if not a.startswith("--out=")] or ["C1", "C2"]
-    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    args = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2"]
+    opt = dict(a[2:].split("=", 1) for a in sys.argv[1:] if a.startswith("--"))
     ms = (10, 20) if all(a in ("C1", "C2") for a in args) else (20,)
-    main(args, ms, outs[0] if outs else None)
+    main(args, ms, opt.get("out"), opt.get("store"))

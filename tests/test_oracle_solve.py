@@ -186,3 +186,24 @@ def test_gmres_jacobi_same_energy_fewer_iterations():
     assert j["report"]["rel_res_true"] <= 1e-9
     assert j["energy"] == pytest.approx(a["energy"], rel=1e-8)
     assert j["report"]["iterations"] <= 0.6 * a["report"]["iterations"]
+
+
+def test_gmres_checkpointed_replays_bitwise(tmp_path):
+    """The product store used for the full-size C4 golden (tests/make_oracle_golden.py --store):
+    same x, history and counts as the plain oracle GMRES, also when resumed from a partial store,
+    and a stored product made from another x is detected."""
+    p = g.sphere_problem(2, 4.0, g.helix_charges())
+    b = oracle.source(p)
+    x0, st0, r0 = oracle.gmres(p, b, restart=10, tol=1e-12)
+    store = str(tmp_path / "store")
+    x1, st1, r1 = oracle.gmres_checkpointed(p, b, store, restart=10, tol=1e-12)
+    assert st1 == st0 and np.array_equal(x0, x1) and np.array_equal(r0["history"], r1["history"])
+    assert r1["matvecs"] == r0["matvecs"] == len(os.listdir(store))
+    files = sorted(os.listdir(store))
+    for f in files[len(files) // 2:]:  # a run cut off half way
+        os.remove(os.path.join(store, f))
+    x2, _, r2 = oracle.gmres_checkpointed(p, b, store, restart=10, tol=1e-12)
+    assert np.array_equal(x0, x2) and r2["iterations"] == r0["iterations"]
+    os.rename(os.path.join(store, files[1]), os.path.join(store, files[1][:4] + "0000000000000000.npy"))
+    with pytest.raises(RuntimeError):
+        oracle.gmres_checkpointed(p, b, store, restart=10, tol=1e-12)
