@@ -177,7 +177,7 @@ def config(name: str) -> Problem:
 
 def random_vector(n2: int, seed: int, smooth_centroids=None):
     """Seeded operand u for matvec parity: U(-1,1) entries, or a smooth field
-    cos(x)+sin(2y)+z evaluated at the centroids (both halves) when given."""
+    f = cos(0.3x) + sin(0.2y) + 0.1z evaluated at the centroids when given (u = [f, f/2])."""
     if smooth_centroids is not None:
         c = smooth_centroids
         f = np.cos(c[:, 0] * 0.3) + np.sin(0.2 * c[:, 1]) + 0.1 * c[:, 2]

@@ -31,9 +31,22 @@
  * broadcast it).  Every rank holds the full geometry and charges, passes and receives
  * full-length vectors, and runs the same (replicated, deterministic) GMRES.  The product is
  * sharded by kernel (bipb_set_matvec_kernel): the row kernel splits target rows
- * (bipb_partition) and an NCCL all-gather reassembles y; the symmetric kernel splits its
- * block schedule (bipb_partition of the 640-row blocks) and an NCCL all-reduce sums the
- * ranks' partial row sums.  Source and energy shard target rows / charges + all-gather.
+ * (bipb_partition); the symmetric kernel splits its block schedule (bipb_partition of the
+ * 640-row blocks) and every rank produces partial sums for all rows -- by default exact
+ * fixed-point limbs (bipb_set_sum_mode), so the P-rank product is bitwise the single-GPU one.
+ * Source and energy shard target rows / charges.  The per-product exchange is, by default,
+ * peer stores into every rank's mailbox (see BIPB_DIST_P2P below), else NCCL collectives.
+ *
+ * Failures of the exchange: a peer that does not deliver within
+ * BIPB_P2P_TIMEOUT_S (default 120 s), an NCCL error, or a synchronisation of a multi-rank context
+ * that takes longer than BIPB_COMM_TIMEOUT_S (default 600 s) returns BIPB_ERR_NCCL (the NCCL
+ * communicator is aborted with ncclCommAbort).  The context is then marked failed: every later
+ * call returns BIPB_ERR_NCCL at once; destroy it.  The process's CUDA context stays usable.
+ *
+ * Stream ordering: the library orders a context's work on the stream given at setup (else a
+ * private non-blocking stream) and each call returns after its work completed.  Device inputs
+ * written on ANOTHER stream must be complete before the call (the Python binding synchronises
+ * torch's current stream when it differs from the context's).
  */
 #ifndef BIPB_H
 #define BIPB_H
@@ -71,8 +84,12 @@ typedef struct {
  * writes its rows / partial sums straight into every rank's mailbox (CUDA IPC mappings over
  * NVLink / NVSwitch, set up once with NCCL all-gathers), then a flag handshake in device
  * memory; used when every rank can map every other rank's memory (up to 16 ranks), else the
- * NCCL collectives (all-gather / all-reduce).  Same values either way (row kernel: bitwise).
- * BIPB_DIST_P2P forces peer stores (ERR_ARG if impossible, also at world 1), BIPB_DIST_NCCL
+ * NCCL collectives (all-gather / all-reduce).  Same values either way (row kernel and exact
+ * sums: bitwise).  At setup every rank opens every peer's mailbox (devices compared by UUID,
+ * not by per-process ordinal) and runs a self-test: each rank stores a known word and flag
+ * into every mailbox, and after a barrier checks what arrived.  Any failure on any rank makes
+ * all ranks use the collectives.  BIPB_DIST_P2P forces peer stores (ERR_NCCL from setup if the
+ * mappings or the self-test fail; ERR_ARG beyond 16 ranks; also at world 1), BIPB_DIST_NCCL
  * forces the collectives; the environment variable BIPB_EXCHANGE=p2p|nccl overrides both. */
 #define BIPB_DIST_P2P 2
 #define BIPB_DIST_NCCL 4
@@ -199,8 +216,10 @@ bipb_status bipb_nccl_unique_id(unsigned char* out);
  *      value is bitwise independent of the launch configuration and of the rank count.
  *   1  symmetric kernel: each unordered pair {i, j} evaluated once and used for both rows
  *      (K1, K4 symmetric; K2/K3 exchange under d -> -d); 27.5 instead of 47 FP64
- *      instructions per ordered pair; deterministic for a fixed rank count; across ranks
- *      the partial products are summed with ncclAllReduce.
+ *      instructions per ordered pair.  Partial sums are added as exact fixed-point limbs by
+ *      default (bipb_set_sum_mode 1: bitwise independent of schedule and rank count), or as
+ *      fixed-order double partials (mode 0: deterministic for a fixed rank count); across
+ *      ranks they travel through the per-product exchange (peer stores or NCCL).
  * Default: 1 when the problem has at least one wave (296) of 640 x 640 tile pairs
  * (N >~ 15k), else 0.  BIPB_MATVEC=row|sym in the environment overrides it at setup.
  */

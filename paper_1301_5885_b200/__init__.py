@@ -116,6 +116,22 @@ def _ptr(a, writable=False, size=None):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _order(ctx, *arrays):
+    """Stream ordering for torch CUDA tensors.  The library runs a context's work on
+    the stream given at setup (else its own non-blocking stream) and returns after completion, so
+    outputs are ready for any stream afterwards.  Inputs produced by torch kernels still queued on
+    torch's current stream must be finished first: when the context does not run on that very
+    stream, synchronise it before the call."""
+    for a in arrays:
+        if a is None or isinstance(a, np.ndarray) or not getattr(a, "is_cuda", False):
+            continue
+        import torch
+        cur = torch.cuda.current_stream(a.device)
+        if ctx._stream is None or int(ctx._stream) != int(cur.cuda_stream):
+            cur.synchronize()
+        return
+
+
 def version() -> str:
     return _lib.bipb_version().decode()
 
@@ -135,10 +151,11 @@ def bipb_nccl_unique_id() -> bytes:
 class Context:
     """Owns a bipb_ctx (device geometry, charges, buffers, stream, NCCL comm)."""
 
-    def __init__(self, handle, n, nc, keep):
+    def __init__(self, handle, n, nc, keep, stream=None):
         self._h = handle
         self.n, self.nc = n, nc
         self._keep = keep
+        self._stream = stream  # the cudaStream_t the library runs this context on (None: its own)
 
     @property
     def handle(self):
@@ -226,7 +243,7 @@ def bipb_setup(centroids, normals, areas, charges, eps1, eps2, kappa, dist=None,
     st = _lib.bipb_setup(ctypes.byref(h), n, pc, pn, pa, nc, pq, float(eps1), float(eps2), float(kappa),
                          ctypes.byref(d) if d is not None else None, stream)
     _check(st)
-    return Context(h, n, nc, (kc, kn, ka, kq))
+    return Context(h, n, nc, (kc, kn, ka, kq), stream)
 
 
 def _out_like(ctx_n2, like):
@@ -239,6 +256,7 @@ def bipb_source(ctx: Context, b=None):
     """Eq. (11): b = [S1; S2] (2n).  Returns b (a new numpy array if b is None)."""
     b = _out_like(2 * ctx.n, b)
     pb, _ = _ptr(b, writable=True, size=2 * ctx.n)
+    _order(ctx, b)
     _check(_lib.bipb_source(ctx.handle, pb))
     return b
 
@@ -248,6 +266,7 @@ def bipb_matvec(ctx: Context, u, y=None):
     y = _out_like(2 * ctx.n, y)
     pu, _ = _ptr(u, size=2 * ctx.n)
     py, _ = _ptr(y, writable=True, size=2 * ctx.n)
+    _order(ctx, u, y)
     _check(_lib.bipb_matvec(ctx.handle, pu, py))
     return y
 
@@ -259,6 +278,7 @@ def bipb_matvec_batch(ctx: Context, U, Y=None):
         Y = np.empty((nrhs, 2 * ctx.n))
     pu, _ = _ptr(U, size=nrhs * 2 * ctx.n)
     py, _ = _ptr(Y, writable=True, size=nrhs * 2 * ctx.n)
+    _order(ctx, U, Y)
     _check(_lib.bipb_matvec_batch(ctx.handle, nrhs, pu, py))
     return Y
 
@@ -267,6 +287,7 @@ def bipb_set_charges(ctx: Context, charges):
     """Replace the point charges [nc, 4] (x, y, z, Q) on the same surface."""
     nc = int(charges.shape[0])
     pq, _ = _ptr(charges, size=4 * nc) if nc > 0 else (None, None)
+    _order(ctx, charges)
     _check(_lib.bipb_set_charges(ctx.handle, nc, pq))
     ctx.nc = nc
 
@@ -284,6 +305,7 @@ def bipb_gmres_solve_batch(ctx: Context, B, X, restart_m=20, tol=1e-10, max_iter
         reps[r].history_cap = cap
     pb, _ = _ptr(B, size=nrhs * 2 * ctx.n)
     px, _ = _ptr(X, writable=True, size=nrhs * 2 * ctx.n)
+    _order(ctx, B, X)
     st = _lib.bipb_gmres_solve_batch(ctx.handle, nrhs, pb, px, int(restart_m), float(tol), int(max_iters),
                                      int(check_true), reps)
     if st not in (OK, NOT_CONVERGED):
@@ -306,6 +328,7 @@ def bipb_gmres_solve(ctx: Context, x, b=None, restart_m=20, tol=1e-10, max_iters
     cap = max_iters + 1 if history_cap is None else history_cap
     hist = np.zeros(max(cap, 1))
     rep = Report(history=hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap=cap)
+    _order(ctx, x, b)
     st = _lib.bipb_gmres_solve(ctx.handle, pb, px, int(restart_m), float(tol), int(max_iters), int(check_true),
                                ctypes.byref(rep))
     if st not in (OK, NOT_CONVERGED) or (st == NOT_CONVERGED and raise_on_not_converged):
@@ -320,6 +343,7 @@ def bipb_energy(ctx: Context, x, phi_reac=None) -> float:
     px, _ = _ptr(x, size=2 * ctx.n)
     e = np.zeros(1)
     pp, _ = _ptr(phi_reac, writable=True, size=ctx.nc) if phi_reac is not None else (None, None)
+    _order(ctx, x, phi_reac)
     _check(_lib.bipb_energy(ctx.handle, px, e.ctypes.data, pp))
     return float(e[0])
 
@@ -348,7 +372,7 @@ def bipb_get_precond(ctx: Context) -> int:
 
 
 def bipb_set_sum_mode(ctx: Context, mode: int):
-    """0 = fixed-order double partials (default), 1 = exact fixed-point sums (bipb.h)."""
+    """1 = exact fixed-point limb sums (the default), 0 = fixed-order double partials (bipb.h)."""
     ctx.set_sum_mode(mode)
 
 

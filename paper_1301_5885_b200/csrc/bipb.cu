@@ -12,6 +12,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bipb.h"
@@ -104,6 +105,9 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // failure handling (optional symbols: the one-GPU test stand-in has neither)
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   bool ok = false;
 };
 static NcclApi load_nccl() {
@@ -123,6 +127,8 @@ static NcclApi load_nccl() {
     api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+    api.CommAbort = (decltype(api.CommAbort))dlsym(api.h, "ncclCommAbort");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(api.h, "ncclCommGetAsyncError");
     api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce && api.CommDestroy &&
              api.GetErrorString;
   }
@@ -216,7 +222,14 @@ struct bipb_ctx {
   PeerBoxes boxes{};
   PeerFlags flags{};
   std::vector<void*> p2p_opened;  // peer mappings to close
-  unsigned long long p2p_timeout_ns = 120ull * 1000000000ull;
+  unsigned long long p2p_timeout_ns = 120ull * 1000000000ull;  // peer-store delivery (BIPB_P2P_TIMEOUT_S)
+  unsigned long long comm_timeout_ns = 600ull * 1000000000ull; // host watchdog (BIPB_COMM_TIMEOUT_S)
+  unsigned int* p2p_err = nullptr;      // mapped pinned word: 1 + rank that missed a delivery (p2p_wait_kernel)
+  unsigned int* p2p_err_dev = nullptr;  // its device address
+  // a peer that missed a delivery or a failed / stuck collective leaves the context unusable: every
+  // later call returns BIPB_ERR_NCCL with this message (destroy the context)
+  bool failed = false;
+  std::string failed_msg;
 
   bool timing = false;
   EventPool pool[3];
@@ -359,9 +372,23 @@ static void dfree(bipb_ctx* c, void* p) {
   if (p) cudaFreeAsync(p, c->stream);
 }
 
+static void drop_graphs(bipb_ctx* c) {
+  if (c->stream) cudaStreamSynchronize(c->stream);  // no replay of them is still pending
+  for (auto e : c->ag.ex)
+    if (e) cudaGraphExecDestroy(e);
+  c->ag.ex.clear();
+  c->ag.V = nullptr;  // forces a rebuild on the next solve
+}
+
+// chunk-partial scratch of the row kernel / source / energy, grown on demand.  A reallocation
+// invalidates the cached Arnoldi-step graphs, which bake the old pointer into their row-kernel
+// products (a replay would otherwise write into freed pool memory).
 static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
   if (doubles <= c->part_cap) return BIPB_OK;
-  if (c->part) dfree(c, c->part);
+  if (c->part) {
+    drop_graphs(c);
+    dfree(c, c->part);
+  }
   c->part = nullptr;
   CK(dmalloc(c, &c->part, doubles * sizeof(double)));
   c->part_cap = doubles;
@@ -377,6 +404,77 @@ static bipb_status ensure_part(bipb_ctx* c, size_t doubles) {
     CK(cudaGetLastError());                                         \
   } while (0)
 
+static void p2p_teardown(bipb_ctx* c) {
+  cudaStreamSynchronize(c->stream);
+  for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
+  c->p2p_opened.clear();
+  if (c->p2p_box) cudaFree(c->p2p_box);
+  if (c->p2p_flags) cudaFree(c->p2p_flags);
+  c->p2p_box = nullptr;
+  c->p2p_flags = nullptr;
+  c->boxes = PeerBoxes{};
+  c->flags = PeerFlags{};
+  cudaGetLastError();
+}
+
+
+// ---- failure handling of the multi-GPU exchange (SURVEY.md §5 "failure detection")
+// Marks the context failed; aborts the communicator so NCCL kernels still waiting on a peer exit.
+static bipb_status ctx_fail(bipb_ctx* c, const std::string& msg) {
+  if (!c->failed) {
+    c->failed = true;
+    c->failed_msg = msg;
+    if (c->comm && nccl().CommAbort) {
+      nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+    }
+  }
+  return fail(BIPB_ERR_NCCL, msg);
+}
+static bipb_status nccl_check(bipb_ctx* c, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return BIPB_OK;
+  return ctx_fail(c, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+static bipb_status check_alive(bipb_ctx* c) {
+  if (c->failed) return fail(BIPB_ERR_NCCL, "context failed earlier (" + c->failed_msg + "); destroy it");
+  return BIPB_OK;
+}
+static bipb_status p2p_check(bipb_ctx* c) {
+  if (c->p2p && c->p2p_err && *reinterpret_cast<volatile unsigned int*>(c->p2p_err) != 0u)
+    return ctx_fail(c, "peer-store exchange: rank " + std::to_string(*c->p2p_err - 1) + " did not deliver within " +
+                           std::to_string(c->p2p_timeout_ns / 1000000000ull) + " s (BIPB_P2P_TIMEOUT_S)");
+  return BIPB_OK;
+}
+// Wait for the context's stream.  Single-GPU contexts block in cudaStreamSynchronize.  Sharded
+// contexts poll: an NCCL asynchronous error, or stream work still running after the host watchdog
+// (BIPB_COMM_TIMEOUT_S, default 600 s per synchronisation -- far above one product: C5 on one GPU
+// takes 8.6 s) aborts the communicator and returns BIPB_ERR_NCCL instead of hanging; a missed
+// peer-store delivery is reported from the wait kernel's error word.
+static bipb_status ctx_sync(bipb_ctx* c) {
+  if (!c->sharded || c->no_comm) {
+    CK(cudaStreamSynchronize(c->stream));
+    return BIPB_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int spins = 0;
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) CK(e);
+    if (c->comm && nccl().CommGetAsyncError) {
+      ncclResult_t ar = ncclSuccess;
+      if (nccl().CommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+        return ctx_fail(c, std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ar));
+    }
+    const auto el = std::chrono::steady_clock::now() - t0;
+    if ((unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(el).count() > c->comm_timeout_ns)
+      return ctx_fail(c, "exchange did not complete within BIPB_COMM_TIMEOUT_S (" +
+                             std::to_string(c->comm_timeout_ns / 1000000000ull) + " s)");
+    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  return p2p_check(c);
+}
+
 // exchange: every rank's rows [r0,r1) of the two halves -> full vector on every rank
 static bipb_status allgather_rows(bipb_ctx* c, double* y) {
   if (c->no_comm) {  // test mode: place this rank's rows only
@@ -388,8 +486,8 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
     return BIPB_OK;
   }
   NcclApi& api = nccl();
-  ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)(2 * c->np), ncclFloat64, c->comm, c->stream);
-  if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+  CKS(nccl_check(c, api.AllGather(c->stage, c->gather, (size_t)(2 * c->np), ncclFloat64, c->comm, c->stream),
+                 "ncclAllGather"));
   LAUNCH1D(unpack_kernel, c->world * c->np, c->gather, c->n, c->np, c->world, y);
   return BIPB_OK;
 }
@@ -398,7 +496,8 @@ static bipb_status allgather_rows(bipb_ctx* c, double* y) {
 // every rank's mailbox; publish the epoch and wait for every rank's delivery.
 static bipb_status p2p_publish_and_wait(bipb_ctx* c) {
   p2p_signal_kernel<<<1, 32, 0, c->stream>>>(c->p2p_epoch, c->flags, c->world, c->rank);
-  p2p_wait_kernel<<<1, 32, 0, c->stream>>>(c->p2p_epoch, c->p2p_flags, c->world, c->p2p_timeout_ns);
+  p2p_wait_kernel<<<1, 32, 0, c->stream>>>(c->p2p_epoch, c->p2p_flags, c->world, c->p2p_timeout_ns,
+                                            c->p2p_err_dev);
   c->launches_all += 2;
   CK(cudaGetLastError());
   return BIPB_OK;
@@ -465,7 +564,7 @@ static bipb_status exact_overflowed(bipb_ctx* c, bool* out) {
   if (!c->xsticky) return BIPB_OK;
   int h = 0;
   CK(cudaMemcpyAsync(&h, c->xsticky, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   if (h) {
     CK(cudaMemsetAsync(c->xsticky, 0, sizeof(int), c->stream));
     c->exact_off = true;
@@ -567,9 +666,8 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y, bool al
                c->p2p_epoch, c->world, xwords, c->xexp, c->xbias, U, n, d1, d2, Y, c->xsticky);
     } else {
       if (c->sharded && !c->no_comm) {  // integer sums: exact in any reduction order
-        NcclApi& api = nccl();
-        ncclResult_t r = api.AllReduce(c->xl, c->xl, (size_t)xwords, ncclUint64, ncclSum, c->comm, c->stream);
-        if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+        CKS(nccl_check(c, nccl().AllReduce(c->xl, c->xl, (size_t)xwords, ncclUint64, ncclSum, c->comm, c->stream),
+                       "ncclAllReduce"));
       }
       LAUNCH1D(finish_exact_kernel, 2 * n, c->xl, 0, nullptr, 1, xwords, c->xexp, c->xbias, U, n, d1, d2, Y,
                c->xsticky);
@@ -584,10 +682,9 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y, bool al
     return BIPB_OK;
   }
   if (c->sharded && !c->no_comm) {  // every rank holds partial sums for all rows
-    NcclApi& api = nccl();
-    ncclResult_t r =
-        api.AllReduce(c->sym_P, c->sym_P, (size_t)(R * 2 * n), ncclFloat64, ncclSum, c->comm, c->stream);
-    if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    CKS(nccl_check(c, nccl().AllReduce(c->sym_P, c->sym_P, (size_t)(R * 2 * n), ncclFloat64, ncclSum, c->comm,
+                                       c->stream),
+                   "ncclAllReduce"));
   }
   LAUNCH1D(finish_sym_kernel<R>, n, c->sym_P, U, n, d1, d2, Y);
   c->matvec_calls += R;
@@ -648,7 +745,7 @@ static bipb_status dot_dev(bipb_ctx* c, const double* a, const double* b, int64_
 
 static bipb_status read_scalars(bipb_ctx* c, const double* dsrc, int count, double* host) {
   CK(cudaMemcpyAsync(c->host_info, dsrc, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   memcpy(host, c->host_info, sizeof(double) * count);
   return BIPB_OK;
 }
@@ -730,15 +827,19 @@ void bipb_destroy(bipb_ctx* c) {
   if (c->xsticky) dfree(c, c->xsticky);
   if (c->p2p_epoch) dfree(c, c->p2p_epoch);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
-  if (c->p2p_box) cudaFree(c->p2p_box);
-  if (c->p2p_flags) cudaFree(c->p2p_flags);
+  p2p_teardown(c);
+  if (c->p2p_err) cudaFreeHost(c->p2p_err);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (auto& p : c->pool)
     for (auto e : p.ev) cudaEventDestroy(e);
   for (auto e : c->ag.ex)
     if (e) cudaGraphExecDestroy(e);
-  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->comm && nccl().ok) {
+    if (c->failed && nccl().CommAbort)
+      nccl().CommAbort(c->comm);
+    else
+      nccl().CommDestroy(c->comm);
+  }
   if (c->stream) cudaStreamSynchronize(c->stream);  // the stream-ordered frees have completed
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -798,80 +899,140 @@ static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<doubl
 }
 
 // Peer-store exchange (bipb_p2p.cuh): mailbox + flags in cudaMalloc memory (IPC-exportable),
-// handles all-gathered once over the communicator and opened on every rank.  `require`: fail
-// unless every rank can map every other rank's memory; otherwise (auto) a rank pair without
-// peer access makes ALL ranks keep the NCCL collectives (the decision is all-gathered).
+// handles all-gathered once over the communicator, opened on every rank and SELF-TESTED before
+// first use.  Devices are identified by UUID: ordinals are per process (under per-rank
+// CUDA_VISIBLE_DEVICES every rank sees its own GPU as device 0).  Any failure on any rank -- a
+// visible peer GPU without P2P access, an IPC handle that does not open, a probe word or flag that
+// does not arrive -- is all-gathered, and then ALL ranks keep the NCCL collectives (auto) or setup
+// fails (`require`: BIPB_DIST_P2P / BIPB_EXCHANGE=p2p).  BIPB_P2P_PROBE_FAIL=<rank> makes that
+// rank report a failed probe (tests of the fallback).
 static bipb_status p2p_setup(bipb_ctx* c, bool require) {
-  if (c->world > P2P_MAX) return fail(BIPB_ERR_ARG, "the peer-store exchange supports up to 16 ranks");
-  if (const char* e = getenv("BIPB_P2P_TIMEOUT_S")) c->p2p_timeout_ns = (unsigned long long)(atof(e) * 1e9);
+  if (c->world > P2P_MAX) {
+    if (require) return fail(BIPB_ERR_ARG, "the peer-store exchange supports up to 16 ranks");
+    return BIPB_OK;  // NCCL collectives
+  }
   const int64_t m2 = 2 * c->n;
-  c->p2p_stride = (int64_t)c->world * 4 * m2;  // symmetric slots [world][R <= 4][2n]; row kernel [2n]
+  c->p2p_stride = std::max<int64_t>((int64_t)c->world * 4 * m2, c->world);  // slots [world][R <= 4][2n]
   CK(cudaMalloc(&c->p2p_box, 2 * (size_t)c->p2p_stride * sizeof(double)));
   CK(cudaMalloc(&c->p2p_flags, (size_t)c->world * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(c->p2p_flags, 0, (size_t)c->world * sizeof(unsigned long long), c->stream));
-  CK(dmalloc(c, &c->p2p_epoch, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(c->p2p_box, 0, (size_t)c->world * sizeof(unsigned long long), c->stream));
+  if (!c->p2p_epoch) CK(dmalloc(c, &c->p2p_epoch, sizeof(unsigned long long)));
   CK(cudaMemsetAsync(c->p2p_epoch, 0, sizeof(unsigned long long), c->stream));
+  if (!c->p2p_err) {
+    CK(cudaHostAlloc(&c->p2p_err, sizeof(unsigned int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&c->p2p_err_dev, c->p2p_err, 0));
+  }
+  *c->p2p_err = 0u;
   c->boxes.p[c->rank] = c->p2p_box;
   c->flags.p[c->rank] = c->p2p_flags;
   if (c->world > 1) {
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-    constexpr int W = 17;  // per rank: box handle (8 doubles), flags handle (8), device ordinal
+    constexpr int W = 18;  // per rank: box handle (8 doubles), flags handle (8), device UUID (2)
     cudaIpcMemHandle_t hb, hf;
     CK(cudaIpcGetMemHandle(&hb, c->p2p_box));
     CK(cudaIpcGetMemHandle(&hf, c->p2p_flags));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
     double mine[W];
     memcpy(mine, &hb, 64);
     memcpy(mine + 8, &hf, 64);
-    mine[16] = (double)c->device;
+    memcpy(mine + 16, &prop.uuid, 16);
     double *dsend = nullptr, *drecv = nullptr;
     CK(dmalloc(c, &dsend, W * sizeof(double)));
     CK(dmalloc(c, &drecv, (size_t)c->world * W * sizeof(double)));
     std::vector<double> all((size_t)c->world * W);
-    NcclApi& api = nccl();
+    // all-gather of `cnt` doubles per rank; completes only once every rank reached it (a barrier)
     auto allgather = [&](const double* src, int cnt, double* dst) -> bipb_status {
       CK(cudaMemcpyAsync(dsend, src, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      ncclResult_t r = api.AllGather(dsend, drecv, (size_t)cnt, ncclFloat64, c->comm, c->stream);
-      if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather (p2p setup): ") + api.GetErrorString(r));
+      CKS(nccl_check(c, nccl().AllGather(dsend, drecv, (size_t)cnt, ncclFloat64, c->comm, c->stream),
+                     "ncclAllGather (p2p setup)"));
       CK(cudaMemcpyAsync(dst, drecv, (size_t)c->world * cnt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
+      CKS(ctx_sync(c));
+      return BIPB_OK;
+    };
+    auto agree = [&](bool mine_ok, bool* all_ok) -> bipb_status {
+      const double v = mine_ok ? 1.0 : 0.0;
+      std::vector<double> oks((size_t)c->world);
+      CKS(allgather(&v, 1, oks.data()));
+      *all_ok = true;
+      for (double o : oks) *all_ok = *all_ok && o != 0.0;
       return BIPB_OK;
     };
     CKS(allgather(mine, W, all.data()));
-    // can this rank map every peer's memory?  (same device: IPC within the GPU)
-    double ok = 1.0;
-    for (int q = 0; q < c->world; ++q) {
-      const int dq = (int)all[(size_t)q * W + 16];
-      int can = 1;
-      if (dq != c->device && cudaDeviceCanAccessPeer(&can, c->device, dq) != cudaSuccess) can = 0;
-      if (!can) ok = 0.0;
+    // 1. reachability: peers on this GPU (same UUID) always; a peer GPU visible in this process
+    // needs P2P access; a peer GPU not visible here is decided by the IPC open itself
+    std::string why;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    for (int q = 0; q < c->world && why.empty(); ++q) {
+      if (q == c->rank || !memcmp(&all[(size_t)q * W + 16], mine + 16, 16)) continue;
+      for (int d = 0; d < ndev; ++d) {
+        cudaDeviceProp pd;
+        if (cudaGetDeviceProperties(&pd, d) != cudaSuccess || memcmp(&pd.uuid, &all[(size_t)q * W + 16], 16)) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, c->device, d) != cudaSuccess || !can)
+          why = "no P2P access to rank " + std::to_string(q) + "'s GPU";
+      }
     }
-    std::vector<double> oks((size_t)c->world);
-    CKS(allgather(&ok, 1, oks.data()));
-    dfree(c, dsend);
-    dfree(c, drecv);
-    bool all_ok = true;
-    for (double v : oks) all_ok = all_ok && v != 0.0;
-    if (!all_ok) {
-      cudaGetLastError();
-      if (require) return fail(BIPB_ERR_ARG, "BIPB_DIST_P2P: some rank cannot access a peer's memory");
-      CK(cudaFree(c->p2p_box));
-      CK(cudaFree(c->p2p_flags));
-      c->p2p_box = nullptr;
-      c->p2p_flags = nullptr;
-      return BIPB_OK;  // NCCL collectives (c->p2p stays false)
-    }
-    for (int q = 0; q < c->world; ++q) {
+    cudaGetLastError();
+    // 2. open every peer's mailbox and flags
+    for (int q = 0; q < c->world && why.empty(); ++q) {
       if (q == c->rank) continue;
       memcpy(&hb, &all[(size_t)q * W], 64);
       memcpy(&hf, &all[(size_t)q * W + 8], 64);
       void *pb = nullptr, *pf = nullptr;
-      CK(cudaIpcOpenMemHandle(&pb, hb, cudaIpcMemLazyEnablePeerAccess));
-      c->p2p_opened.push_back(pb);
-      CK(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
-      c->p2p_opened.push_back(pf);
+      cudaError_t e1 = cudaIpcOpenMemHandle(&pb, hb, cudaIpcMemLazyEnablePeerAccess);
+      if (e1 == cudaSuccess) c->p2p_opened.push_back(pb);
+      cudaError_t e2 = e1 == cudaSuccess ? cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess) : e1;
+      if (e1 == cudaSuccess && e2 == cudaSuccess) c->p2p_opened.push_back(pf);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        cudaGetLastError();
+        why = "cudaIpcOpenMemHandle of rank " + std::to_string(q) + ": " +
+              cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
+        break;
+      }
       c->boxes.p[q] = static_cast<double*>(pb);
       c->flags.p[q] = static_cast<unsigned long long*>(pf);
     }
+    bool all_ok = false;
+    CKS(agree(why.empty(), &all_ok));
+    // 3. probe: every rank stores a known word into every mailbox and a flag into every flag
+    // array; after a barrier each rank checks what arrived in its own memory
+    if (all_ok) {
+      const unsigned long long magic = 0x5EED000000000000ull;
+      p2p_probe_kernel<<<1, 32, 0, c->stream>>>(c->boxes, c->flags, c->world, c->rank, magic);
+      CK(cudaGetLastError());
+      double dummy = 0.0;
+      std::vector<double> bar((size_t)c->world);
+      CKS(allgather(&dummy, 1, bar.data()));
+      std::vector<unsigned long long> words((size_t)c->world), fl((size_t)c->world);
+      CK(cudaMemcpyAsync(words.data(), c->p2p_box, (size_t)c->world * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(fl.data(), c->p2p_flags, (size_t)c->world * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int q = 0; q < c->world && why.empty(); ++q)
+        if (words[q] != p2p_probe_word(q, c->rank) || fl[q] != magic + (unsigned long long)q)
+          why = "probe from rank " + std::to_string(q) + " did not arrive";
+      if (const char* pf = getenv("BIPB_P2P_PROBE_FAIL"))
+        if (atoi(pf) == c->rank && why.empty()) why = "probe failure forced (BIPB_P2P_PROBE_FAIL)";
+      CKS(agree(why.empty(), &all_ok));
+    }
+    dfree(c, dsend);
+    dfree(c, drecv);
+    if (!all_ok) {
+      p2p_teardown(c);
+      if (require)
+        return fail(BIPB_ERR_NCCL, "BIPB_DIST_P2P: peer-store exchange unavailable" +
+                                       (why.empty() ? std::string(" on another rank") : ": " + why));
+      return BIPB_OK;  // NCCL collectives (c->p2p stays false)
+    }
+    // clean slate (probe words and flags) before a final barrier: no rank signals before every
+    // rank has cleared its flags
+    CK(cudaMemsetAsync(c->p2p_flags, 0, (size_t)c->world * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->p2p_box, 0, (size_t)c->world * sizeof(unsigned long long), c->stream));
+    double dummy = 0.0;
+    std::vector<double> bar((size_t)c->world);
+    CKS(allgather(&dummy, 1, bar.data()));
   }
   CK(cudaStreamSynchronize(c->stream));
   c->p2p = true;
@@ -933,6 +1094,8 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   if (const char* pe = getenv("BIPB_PRECOND")) c->precond = (!strcmp(pe, "jacobi") || !strcmp(pe, "1")) ? 1 : 0;
   if (const char* se = getenv("BIPB_SUM")) c->sum_mode = (!strcmp(se, "fixed") || !strcmp(se, "0")) ? 0 : 1;
   if (const char* xb = getenv("BIPB_EXACT_BIAS")) c->xbias = atoi(xb);
+  if (const char* e = getenv("BIPB_P2P_TIMEOUT_S")) c->p2p_timeout_ns = (unsigned long long)(atof(e) * 1e9);
+  if (const char* e = getenv("BIPB_COMM_TIMEOUT_S")) c->comm_timeout_ns = (unsigned long long)(atof(e) * 1e9);
   c->screened = kappa > 0.0;
   c->s = c->screened ? kappa : 1.0;
   c->rank = dist ? dist->rank : 0;
@@ -1028,8 +1191,7 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
     if (!api.ok) return fail(BIPB_ERR_NCCL, "libnccl.so.2 not loadable");
     ncclUniqueId id;
     memcpy(&id, dist->nccl_uid, 128);
-    ncclResult_t r = api.CommInitRank(&c->comm, c->world, id, c->rank);
-    if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+    CKS(nccl_check(c, api.CommInitRank(&c->comm, c->world, id, c->rank), "ncclCommInitRank"));
     // per-product exchange: peer stores (default when world > 1 and every rank can map every
     // peer) or NCCL collectives; flags BIPB_DIST_P2P / BIPB_DIST_NCCL and BIPB_EXCHANGE=p2p|nccl
     // force one
@@ -1073,6 +1235,7 @@ bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const
 
 bipb_status bipb_source(bipb_ctx* c, double* b) {
   if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
+  CKS(check_alive(c));
   const int64_t n = c->n;
   if (c->nc == 0) {
     CK(cudaMemsetAsync(c->b, 0, 2 * n * sizeof(double), c->stream));
@@ -1105,12 +1268,13 @@ bipb_status bipb_source(bipb_ctx* c, double* b) {
   if (b) {
     CK(cudaMemcpyAsync(b, c->b, 2 * n * sizeof(double), cudaMemcpyDefault, c->stream));
   }
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   return BIPB_OK;
 }
 
 bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
   if (!c || !u || !y) return fail(BIPB_ERR_ARG, "NULL argument");
+  CKS(check_alive(c));
   if (u == y) return fail(BIPB_ERR_ARG, "u and y must not alias");
   const int64_t m2 = 2 * c->n;
   const double* ud;
@@ -1125,7 +1289,7 @@ bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
   if (exact) CKS(exact_overflowed(c, &ovf));
   if (ovf) CKS(matvec_dev(c, ud, yd));  // out-of-range partial: the fixed-order double partials
   if (!ydev) CK(cudaMemcpyAsync(y, yd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   return BIPB_OK;
 }
 
@@ -1260,7 +1424,7 @@ static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
   } else {
     CKS(enqueue_arnoldi_step(c, k, m));
   }
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   h2[0] = c->host_info[0];
   h2[1] = c->host_info[1];
   return BIPB_OK;
@@ -1442,7 +1606,7 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
       if (q.rep) q.rep->rel_res_true = h2[0] / q.beta_b;
     }
   }
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   *n_not_conv = 0;
   for (int r = 0; r < R; ++r) {
     GmresSys& q = sy[r];
@@ -1464,6 +1628,7 @@ bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t re
                              int32_t max_iters, int32_t check_true, bipb_report* rep) {
   if (!c || !x) return fail(BIPB_ERR_ARG, "NULL argument");
   if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
+  CKS(check_alive(c));
   if (!b && !c->have_b) return fail(BIPB_ERR_ARG, "b is NULL and bipb_source has not been called");
   const int64_t m2 = 2 * c->n;
   const int m = restart_m;
@@ -1567,7 +1732,7 @@ rerun:
     }
   }
   if (!xdev) CK(cudaMemcpyAsync(x, xd, m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   if (rep) {
     rep->iterations = its;
     rep->restarts = restarts;
@@ -1584,6 +1749,7 @@ rerun:
 bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, double* X, int32_t restart_m,
                                    double tol, int32_t max_iters, int32_t check_true, bipb_report* reps) {
   if (!c || !B || !X || nrhs < 1) return fail(BIPB_ERR_ARG, "NULL argument or nrhs < 1");
+  CKS(check_alive(c));
   if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
   const int64_t m2 = 2 * c->n;
   bool bdev, xdev;
@@ -1609,7 +1775,8 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
                                     &not_conv);
   if (st == BIPB_OK && !xdev)
     CK(cudaMemcpyAsync(X, xst, (size_t)nrhs * m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  cudaStreamSynchronize(c->stream);
+  if (st == BIPB_OK) st = ctx_sync(c);
+  else cudaStreamSynchronize(c->stream);
   if (bst) dfree(c, bst);
   if (xst) dfree(c, xst);
   if (st != BIPB_OK) return st;
@@ -1619,6 +1786,7 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
 
 bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi_reac) {
   if (!c || !x || !e_sol) return fail(BIPB_ERR_ARG, "NULL argument");
+  CKS(check_alive(c));
   const int64_t n = c->n, nc = c->nc, m2 = 2 * n;
   double e = 0.0;
   if (nc > 0) {
@@ -1649,9 +1817,8 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
         CK(cudaMemcpyAsync(c->gather + (size_t)c->rank * c->kp, c->stage, kloc * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->stream));
       } else {
-        NcclApi& api = nccl();
-        ncclResult_t r = api.AllGather(c->stage, c->gather, (size_t)c->kp, ncclFloat64, c->comm, c->stream);
-        if (r != ncclSuccess) return fail(BIPB_ERR_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+        CKS(nccl_check(c, nccl().AllGather(c->stage, c->gather, (size_t)c->kp, ncclFloat64, c->comm, c->stream),
+                       "ncclAllGather"));
       }
       LAUNCH1D(unpack1_kernel, c->world * c->kp, c->gather, nc, c->kp, c->world, c->phit);
     }
@@ -1668,12 +1835,13 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
     }
   }
   CK(cudaMemcpyAsync(e_sol, &e, sizeof(double), cudaMemcpyDefault, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   return BIPB_OK;
 }
 
 bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double* Y) {
   if (!c || !U || !Y || nrhs < 1) return fail(BIPB_ERR_ARG, "bad argument");
+  CKS(check_alive(c));
   const int64_t m2 = 2 * c->n;
   bool udev, ydev;
   CKS(vec_where(c, U, &udev));
@@ -1697,12 +1865,13 @@ bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double
     CKS(matvec_batch_dev(c, k, ud, yk));
     if (!ydev) CK(cudaMemcpyAsync(yd, yk, (size_t)k * m2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
-  CK(cudaStreamSynchronize(c->stream));
+  CKS(ctx_sync(c));
   return BIPB_OK;
 }
 
 bipb_status bipb_set_charges(bipb_ctx* c, int64_t nc, const double* charges) {
   if (!c || nc < 0 || (nc > 0 && !charges)) return fail(BIPB_ERR_ARG, "bad argument");
+  CKS(check_alive(c));
   std::vector<double> Q(4 * std::max<int64_t>(nc, 0));
   if (nc > 0) {
     if (is_device_ptr(charges)) {

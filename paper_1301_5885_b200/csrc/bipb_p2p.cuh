@@ -11,7 +11,9 @@
 //   2. p2p_signal_kernel: system-scope fence, epoch += 1, release-store the epoch into flag
 //      [rank] of every rank;
 //   3. p2p_wait_kernel: acquire-spin until every rank's flag in the OWN flag array reached the
-//      epoch (a peer that never arrives traps after BIPB_P2P_TIMEOUT_S seconds);
+//      epoch.  A peer that never arrives within BIPB_P2P_TIMEOUT_S seconds sets an error word in
+//      mapped host memory and the kernel returns (no trap: the CUDA context stays usable); the
+//      host turns the word into BIPB_ERR_NCCL and marks the context failed;
 //   4. the consumer kernel reads the own mailbox (row kernel: copy y; symmetric kernel: sum the
 //      ranks' slots in rank order, so every rank gets bitwise the same y).
 // The mailbox parity alternates with the epoch so a fast rank can never overwrite a slot a slow
@@ -118,10 +120,13 @@ __global__ void p2p_signal_kernel(unsigned long long* epoch, const PeerFlags fla
   for (int p = 0; p < world; ++p) st_release_sys(flags.p[p] + rank, e);
 }
 
-// wait until every rank delivered the current epoch into this rank's mailbox
+// wait until every rank delivered the current epoch into this rank's mailbox.  err (mapped host
+// memory): 0 while healthy; on a timeout 1 + the rank that did not deliver.  Once set, later
+// waits return at once (the exchange protocol is broken; the host fails the context).
 __global__ void p2p_wait_kernel(const unsigned long long* epoch, const unsigned long long* my_flags, int world,
-                                unsigned long long timeout_ns) {
+                                unsigned long long timeout_ns, unsigned int* err) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*reinterpret_cast<volatile unsigned int*>(err) != 0u) return;
   const unsigned long long e = *epoch;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -130,13 +135,29 @@ __global__ void p2p_wait_kernel(const unsigned long long* epoch, const unsigned 
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > timeout_ns) {
-        printf("bipb p2p exchange: rank %d did not deliver epoch %llu within the timeout\n", p, e);
-        __trap();
+        atomicExch(err, 1u + static_cast<unsigned int>(p));
+        __threadfence_system();
+        return;
       }
       __nanosleep(200);
     }
   }
   __threadfence_system();
+}
+
+// Setup self-test of the mappings: this rank writes probe_word(rank, p) into word [rank] of every
+// rank p's mailbox and `magic + rank` into flag [rank] of every rank p.  After a barrier each rank
+// checks its own mailbox and flags on the host (p2p_setup).
+__host__ __device__ inline unsigned long long p2p_probe_word(int from, int to) {
+  return 0xB1B0C0DE00000000ull ^ (static_cast<unsigned long long>(from) << 16) ^ static_cast<unsigned long long>(to);
+}
+__global__ void p2p_probe_kernel(const PeerBoxes box, const PeerFlags flags, int world, int rank,
+                                 unsigned long long magic) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int p = 0; p < world; ++p)
+    reinterpret_cast<unsigned long long*>(box.p[p])[rank] = p2p_probe_word(rank, p);
+  __threadfence_system();
+  for (int p = 0; p < world; ++p) st_release_sys(flags.p[p] + rank, magic + static_cast<unsigned long long>(rank));
 }
 
 // row kernel consumer: y = own mailbox (current parity), 2n doubles

@@ -129,5 +129,19 @@ ncclResult_t ncclCommDestroy(ncclComm_t comm) {
   delete c;
   return ncclSuccess;
 }
+// abort: local teardown without the barrier (the peers may be gone or stuck)
+ncclResult_t ncclCommAbort(ncclComm_t comm) {
+  Comm* c = (Comm*)comm;
+  for (int p = 0; p < c->n; ++p)
+    if (p != c->rank) cudaIpcCloseMemHandle(c->peer[p]);
+  cudaFree(c->mine);
+  munmap(c->sh, sizeof(Shared));
+  delete c;
+  return ncclSuccess;
+}
+ncclResult_t ncclCommGetAsyncError(ncclComm_t, ncclResult_t* r) {
+  *r = ncclSuccess;  // collectives are synchronous here: errors are returned directly
+  return ncclSuccess;
+}
 const char* ncclGetErrorString(ncclResult_t r) { return r == ncclSuccess ? "fake nccl: success" : "fake nccl: error"; }
 }

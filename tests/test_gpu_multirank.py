@@ -4,14 +4,19 @@ NCCL refuses two ranks on one device), or through the peer-store exchange (CUDA 
 bipb_p2p.cuh).  Every rank runs the full pipeline (source -> replicated GMRES with one
 collective per product -> energy) and must reproduce the single-GPU results: bitwise for the
 row kernel (rank-count invariant sums), to rounding for the symmetric kernel (all-reduce of
-partial sums)."""
+partial sums).  Every rank's results are also checked against the ORACLE (oracle/, computed once
+in the parent process; the C2 solve from the stored tests/golden/oracle_C2.json): matvec and
+source element-wise and per block, E_sol to 1e-8, iterations +-1, solution rows."""
+import json
 import multiprocessing as mp
 import os
+import time
 
 import numpy as np
 import pytest
 
 import bipb_inputs as g
+import oracle
 
 pytestmark = pytest.mark.gpu
 FAKE = os.path.join(os.path.dirname(__file__), "fakenccl", "libfakenccl.so")
@@ -20,7 +25,45 @@ FAKE = os.path.join(os.path.dirname(__file__), "fakenccl", "libfakenccl.so")
 def _problem(size="big"):
     if size == "tiny":  # 20 elements, 3 charges: most ranks own no rows, blocks or charges
         return g.sphere_problem(0, 4.0, g.charges_in_ball(3, 2.0, 5))
-    return g.sphere_problem(5, 4.0, g.charges_in_ball(30, 3.0, 17))  # N = 20480 (symmetric default)
+    return g.config("C2")  # N = 20480 (symmetric default), the stored oracle solve exists
+
+
+_ORC = {}
+
+
+def _oracle(size):
+    """Oracle values for the pipeline _run executes (u = random_vector(2N, 5), GMRES(20) to 1e-10)."""
+    if size not in _ORC:
+        p = _problem(size)
+        u = g.random_vector(2 * p.n, 5)
+        o = {"y": oracle.matvec(p, u), "b": oracle.source(p)}
+        if size == "tiny":
+            x, st, rep = oracle.gmres(p, o["b"], restart=20, tol=1e-10, max_iters=300)
+            o.update(e=oracle.energy(p, x), its=rep["iterations"], rows=np.arange(p.n), x_phi=x[:p.n],
+                     x_dphi=x[p.n:], x_norm=float(np.linalg.norm(x)))
+        else:
+            gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_C2.json")))
+            assert gold["sha256"] == p.sha256()
+            s20 = gold["solves"]["20"]
+            o.update(e=s20["energy"], its=s20["iterations"], rows=np.array(s20["rows"]),
+                     x_phi=np.array(s20["x_phi"]), x_dphi=np.array(s20["x_dphi"]), x_norm=s20["x_norm"])
+        _ORC[size] = o
+    return _ORC[size]
+
+
+def _check_oracle(o, orc, n):
+    """One rank's outputs against the oracle at the north_star tolerances."""
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    assert rel(o["y"], orc["y"]) <= 1e-11
+    for blk in (slice(0, n), slice(n, 2 * n)):
+        assert rel(o["y"][blk], orc["y"][blk]) <= 1e-11
+        if np.any(orc["b"][blk]):
+            assert rel(o["b"][blk], orc["b"][blk]) <= 1e-12
+    assert abs(o["its"] - orc["its"]) <= 1
+    assert o["e"] == pytest.approx(orc["e"], rel=1e-8)
+    rows = orc["rows"]
+    np.testing.assert_allclose(o["x"][rows], orc["x_phi"], rtol=1e-7, atol=1e-9 * orc["x_norm"])
+    np.testing.assert_allclose(o["x"][rows + n], orc["x_dphi"], rtol=1e-7, atol=1e-9 * orc["x_norm"])
 
 
 def _run(rank, world, uid, kind, exchange, q, size="big", sum_mode="fixed"):
@@ -82,7 +125,9 @@ def test_multirank_matches_single(world, kind, exchange):
     ref = _spawn(0, kind)[0]
     outs = _spawn(world, kind, exchange)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-    for o in outs:  # every rank holds the full, identical result
+    orc, n = _oracle("big"), _problem().n
+    for o in outs:  # every rank holds the full, identical result, equal to the oracle's
+        _check_oracle(o, orc, n)
         assert np.array_equal(o["x"], outs[0]["x"]) and o["e"] == outs[0]["e"]
         assert o["its"] == ref["its"] and o["its_p"] == ref["its_p"] < ref["its"]
         assert np.array_equal(o["xp"], outs[0]["xp"])
@@ -104,7 +149,9 @@ def test_multirank_tiny_problem(kind, exchange):
     still take part in every exchange (zero contributions) and end with the single-GPU result."""
     ref = _spawn(0, kind, size="tiny")[0]
     outs = _spawn(8, kind, exchange, size="tiny")
+    orc, n = _oracle("tiny"), _problem("tiny").n
     for o in outs:
+        _check_oracle(o, orc, n)
         assert o["its"] == ref["its"]
         np.testing.assert_allclose(o["y"], ref["y"], rtol=1e-14, atol=1e-15 * np.abs(ref["y"]).max())
         np.testing.assert_allclose(o["x"], ref["x"], rtol=1e-11, atol=1e-13 * np.abs(ref["x"]).max())
@@ -120,7 +167,116 @@ def test_multirank_exact_sums_bitwise(world, exchange, size):
     energy are bitwise the single-GPU results for every rank count and both exchanges."""
     ref = _spawn(0, 1, size=size, sum_mode="exact")[0]
     outs = _spawn(world, 1, exchange, size=size, sum_mode="exact")
+    orc, n = _oracle(size), _problem(size).n
     for o in outs:
+        _check_oracle(o, orc, n)
         assert np.array_equal(o["y"], ref["y"]) and np.array_equal(o["x"], ref["x"])
         assert o["its"] == ref["its"] and o["e"] == ref["e"]
         assert np.array_equal(o["xp"], ref["xp"])
+
+
+def _run_fail(rank, world, uid, mode, q, done):
+    """Failure paths of the exchange (bipb.cu p2p_setup / ctx_sync): each mode's expectation."""
+    os.environ["BIPB_NCCL_LIB"] = FAKE
+    os.environ["BIPB_GRAPHS"] = "0"
+    if mode == "timeout":  # rank 1 never takes part in the product: rank 0's wait must time out
+        os.environ["BIPB_EXCHANGE"] = "p2p"
+        os.environ["BIPB_P2P_TIMEOUT_S"] = "2"
+    else:  # rank 1's mapping self-test reports a failure
+        os.environ["BIPB_P2P_PROBE_FAIL"] = "1"
+        if mode == "probe_required":
+            os.environ["BIPB_EXCHANGE"] = "p2p"
+    try:
+        import paper_1301_5885_b200 as bp
+        p = _problem("tiny")
+        u = g.random_vector(2 * p.n, 5)
+        dist = (rank, world, uid, 0)
+        if mode == "probe_required":
+            try:
+                bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
+                q.put((rank, None, "setup succeeded although the peer-store exchange was required"))
+            except bp.BipbError as ex:
+                q.put((rank, {"status": ex.status, "msg": str(ex)}, None))
+            return
+        ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
+        if mode == "probe_auto":  # fallback: every rank uses the NCCL collectives, same results
+            res = {"exchange": ctx.exchange, "y": bp.bipb_matvec(ctx, u), "b": bp.bipb_source(ctx)}
+            ctx.close()
+            q.put((rank, res, None))
+            return
+        res = {"exchange": ctx.exchange}
+        if rank == 0:
+            t = time.time()
+            try:
+                bp.bipb_matvec(ctx, u)
+                res["first"] = None
+            except bp.BipbError as ex:
+                res["first"] = (ex.status, str(ex))
+            res["seconds"] = time.time() - t
+            try:
+                bp.bipb_matvec(ctx, u)
+                res["second"] = None
+            except bp.BipbError as ex:
+                res["second"] = (ex.status, str(ex))
+            ctx.close()
+            # the CUDA context survived: a fresh single-GPU context computes the product
+            c1 = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa)
+            res["y_fresh"] = bp.bipb_matvec(c1, u)
+            c1.close()
+            done.set()
+            q.put((rank, res, None))
+        else:
+            done.wait(300)  # keep the mailbox mapped until rank 0 is finished
+            # no ctx.close(): rank 0 aborted the communicator, a destroy would wait for it forever
+            q.put((rank, res, None))
+            q.close()
+            q.join_thread()
+            os._exit(0)
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, None, repr(ex)))
+        done.set()
+
+
+def _spawn_fail(mode, world=2):
+    ctx = mp.get_context("spawn")
+    q, done = ctx.Queue(), ctx.Event()
+    uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
+    procs = [ctx.Process(target=_run_fail, args=(r, world, uid, mode, q, done)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for _, _, err in res:
+        assert err is None, err
+    return [r[1] for r in sorted(res, key=lambda t: t[0])]
+
+
+def test_p2p_timeout_returns_status():
+    """A peer that never delivers: the wait kernel gives up after BIPB_P2P_TIMEOUT_S and the call
+    returns BIPB_ERR_NCCL (no __trap: the process's CUDA context stays usable); the context is then
+    marked failed and later calls return at once."""
+    import paper_1301_5885_b200 as bp
+    r0, r1 = _spawn_fail("timeout")
+    assert r0["exchange"] == r1["exchange"] == "p2p"
+    st, msg = r0["first"]
+    assert st == bp.ERR_NCCL and "did not deliver" in msg and "rank 1" in msg
+    assert 1.5 <= r0["seconds"] < 60
+    st2, msg2 = r0["second"]
+    assert st2 == bp.ERR_NCCL and "failed earlier" in msg2
+    orc = _oracle("tiny")
+    assert np.linalg.norm(r0["y_fresh"] - orc["y"]) <= 1e-11 * np.linalg.norm(orc["y"])
+
+
+def test_p2p_probe_failure_falls_back_to_nccl():
+    """One rank's mapping self-test fails: all ranks agree on the NCCL collectives (auto mode) and
+    still compute the oracle's product and source term; when peer stores are required, setup fails
+    with BIPB_ERR_NCCL on every rank instead."""
+    import paper_1301_5885_b200 as bp
+    orc, n = _oracle("tiny"), _problem("tiny").n
+    for o in _spawn_fail("probe_auto"):
+        assert o["exchange"] == "nccl"
+        assert np.linalg.norm(o["y"] - orc["y"]) <= 1e-11 * np.linalg.norm(orc["y"])
+        np.testing.assert_allclose(o["b"], orc["b"], rtol=1e-12, atol=1e-14 * np.abs(orc["b"]).max())
+    for o in _spawn_fail("probe_required"):
+        assert o["status"] == bp.ERR_NCCL and "peer-store exchange unavailable" in o["msg"]

@@ -131,18 +131,47 @@ def test_solve_parity_golden(bp, cfg):
     ctx.close()
 
 
+@pytest.mark.parametrize("n_keep", [44799, 44800, 44801])
+def test_symmetric_block_edges_b640(bp, n_keep):
+    """Block edges of the bench's block shape B = 640 (chosen once there are >= 2,048 block pairs,
+    N >~ 40k): N = 70*640 - 1, 70*640, 70*640 + 1 (partial last block, nb even / odd).  >= 2,048
+    sampled rows including every 640-row block edge against the oracle (per block), the whole
+    product against the independently pinned row kernel."""
+    p = _ragged(6, 20.0, n_keep, 12, g.charges_in_ball(10, 15.0, 6))
+    ctx = _ctx(bp, p)
+    assert ctx.matvec_kernel == 1 and ctx.sum_mode == 1
+    u = g.random_vector(2 * p.n, 7)
+    y1 = bp.bipb_matvec(ctx, u)
+    ctx.set_matvec_kernel(0)
+    y0 = bp.bipb_matvec(ctx, u)
+    ctx.close()
+    assert _rel(y1, y0) <= 1e-13
+    edges = np.arange(0, p.n + 1, 640)
+    rows = np.unique(np.clip(np.concatenate([edges - 1, edges, np.linspace(0, p.n - 1, 1900).astype(np.int64)]),
+                             0, p.n - 1))
+    assert rows.size >= 2048
+    yi, yin = oracle.matvec_rows(p, u, rows)
+    for got, want in ((y1[rows], yi), (y1[rows + p.n], yin)):
+        assert _rel(got, want) <= 1e-11
+        assert np.max(np.abs(got - want)) <= 1e-11 * np.max(np.abs(want))
+
+
 def test_full_size_c4_sampled(bp):
     """C4 (N = 327,680, the bench workload): sampled rows of the matvec and source, sampled
     charges of phi_reac against the oracle; the solved energy against the Kirkwood series
     (a property that holds at any size: BEM -> Kirkwood with discretisation error ~1e-3)."""
     p = g.config("C4")
     ctx = _ctx(bp, p)
-    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 24).astype(np.int64), [0, 1, 255, 256, p.n - 1]]))
+    # 2,048 sampled rows (SURVEY §8(d)) plus the 640-row block edges near both ends
+    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 2048).astype(np.int64),
+                                     [0, 1, 639, 640, 641, 1279, 1280, p.n - 641, p.n - 640, p.n - 1]]))
+    assert rows.size >= 2048
     u = g.random_vector(2 * p.n, 21)
     y = bp.bipb_matvec(ctx, u)
     yi, yin = oracle.matvec_rows(p, u, rows)
-    assert np.max(np.abs(y[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
-    assert np.max(np.abs(y[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))
+    for got, want in ((y[rows], yi), (y[rows + p.n], yin)):  # per block: rel-L2 and element-wise
+        assert _rel(got, want) <= 1e-11
+        assert np.max(np.abs(got - want)) <= 1e-11 * np.max(np.abs(want))
     b = bp.bipb_source(ctx)
     sub = g.Problem("sub", p.centroids[rows], p.normals[rows], p.areas[rows], p.charges, p.eps1, p.eps2, p.kappa)
     bo = oracle.source(sub)
@@ -341,9 +370,10 @@ def test_symmetric_shards_sum_to_single_gpu(bp, world):
     assert _rel(acc + du, y1) <= 1e-14
 
 
-@pytest.mark.parametrize("n_keep", [1, 2, 511, 512, 513, 1023, 1536, 2047, 2560, 5119])
+@pytest.mark.parametrize("n_keep", [1, 2, 383, 384, 385, 767, 768, 769, 1151, 1536, 2047, 2560, 5119])
 def test_symmetric_block_edges(bp, n_keep):
-    """Ragged block counts (odd/even nb, partial last block, nb = 1, 2) for the circulant schedule."""
+    """Ragged block counts around the mid-size block B = 384 (the shape every N below ~40k gets):
+    nb = 1, 2 with an exactly full / one-row last block, odd and even nb, partial last block."""
     p = _ragged(4, 4.0, n_keep, 3, np.zeros((0, 4))) if n_keep > 1 else g.Problem(
         "n1", np.array([[1.0, 0, 0]]), np.array([[1.0, 0, 0]]), np.array([0.3]), np.zeros((0, 4)))
     ctx = _ctx(bp, p)

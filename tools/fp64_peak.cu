@@ -19,6 +19,11 @@ __global__ void fp64_loop(double* out, int iters, double a, double b) {
         if (OP == 0) x[c] = fma(x[c], (c & 1) ? a : a2, (c & 2) ? b : b2);
         if (OP == 1) x[c] = x[c] * ((c & 1) ? a : a2);
         if (OP == 2) x[c] = x[c] + ((c & 1) ? b : b2);
+        // operand patterns of the DFMA stream: OP 0 reads four distinct source registers across the
+        // chains, OP 3 two multiplicands and one addend (tools/dmma_probe.cu's pattern), OP 4 one
+        // of each -- register-bank conflicts of the 3-operand DFMA separate them (r02 reconciliation)
+        if (OP == 3) x[c] = fma(x[c], (c & 1) ? a : a2, b);
+        if (OP == 4) x[c] = fma(x[c], a, b);
       }
     }
   }
@@ -47,7 +52,7 @@ void run(const char* name, int threads, int blocks_per_sm, int sms, double* out)
     if (ms < best) best = ms;
   }
   double inst = (double)blocks * threads * iters * 16 * CHAINS;
-  double flops = inst * (OP == 0 ? 2.0 : 1.0);
+  double flops = inst * ((OP == 0 || OP >= 3) ? 2.0 : 1.0);
   printf("{\"op\": \"%s\", \"chains\": %d, \"threads\": %d, \"blocks_per_sm\": %d, \"ginst_per_s\": %.1f, "
          "\"tflops\": %.3f, \"inst_per_clk_per_sm_at_1965\": %.2f}\n",
          name, CHAINS, threads, blocks_per_sm, inst / (best * 1e-3) / 1e9, flops / (best * 1e-3) / 1e12,
@@ -67,6 +72,11 @@ int main() {
   run<4, 0>("dfma", 128, 16, S, out);
   run<16, 0>("dfma", 128, 2, S, out);
   run<16, 0>("dfma", 128, 4, S, out);
+  run<8, 3>("dfma_2src", 256, 4, S, out);
+  run<16, 3>("dfma_2src", 256, 4, S, out);
+  run<16, 3>("dfma_2src", 128, 4, S, out);
+  run<8, 4>("dfma_1src", 256, 4, S, out);
+  run<16, 4>("dfma_1src", 256, 4, S, out);
   run<8, 1>("dmul", 256, 4, S, out);
   run<8, 2>("dadd", 256, 4, S, out);
   printf("{\"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));

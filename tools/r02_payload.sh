@@ -1,0 +1,34 @@
+#!/bin/bash
+# GPU payload run beside the C4 oracle golden (tools/c4_golden_box.sh): test suite with a few
+# OpenMP threads for the oracle checks, FP64 peak probes, bench, one full ncu capture of the
+# symmetric kernel (CSV exports only: gpurun_out is capped at 64 MiB with the golden's products).
+# Usage: bash tools/r02_payload.sh TAG [tests|bench|ncu|peak ...]
+set -u
+TAG=${1:-r02}; shift || true
+WHAT=${*:-"tests peak bench ncu"}
+O=gpurun_out/$TAG
+mkdir -p $O
+for w in $WHAT; do
+  case $w in
+    tests)
+      OMP_NUM_THREADS=${PAYLOAD_OMP:-4} timeout ${TEST_TIMEOUT:-2700} python -m pytest tests -m gpu -q -p no:cacheprovider \
+        --timeout 1200 -rfEs > $O/pytest_gpu.txt 2>&1
+      tail -30 $O/pytest_gpu.txt ;;
+    peak)
+      tools/fp64_peak > $O/fp64_peak.jsonl 2>&1; tools/dmma_probe > $O/dmma_probe.jsonl 2>&1 ;;
+    bench)
+      timeout 900 python bench.py --no-cpu-baseline --precond-steps 0 > $O/bench.json 2> $O/bench.err
+      tail -c 3000 $O/bench.json ;;
+    ncu)
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:^sym_kernel -s 1 -c 1 \
+        -o /tmp/prof_sym_$TAG python tools/profile_driver.py C4 2 > $O/ncu_sym.log 2>&1
+      ncu -i /tmp/prof_sym_$TAG.ncu-rep --page raw --csv > $O/prof_sym_raw.csv 2>&1
+      ncu -i /tmp/prof_sym_$TAG.ncu-rep --page source --csv > $O/prof_sym_source.csv 2>&1
+      ncu -i /tmp/prof_sym_$TAG.ncu-rep --page source --csv --print-source sass > $O/prof_sym_sass.csv 2>&1
+      ncu -i /tmp/prof_sym_$TAG.ncu-rep --page details --csv > $O/prof_sym_details.csv 2>&1
+      ls -la $O ;;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+        python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --precond-steps 0 > /dev/null 2>&1 ;;
+  esac
+done
