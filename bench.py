@@ -33,11 +33,16 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # DESIGN.md §6 "Roofline": 37
 # Algorithmic FLOPs per ordered matvec pair-interaction: SURVEY.md §8(d) / App. C F_alg = 60 FLOP
 # (+ 1 exp + 1 rsqrt, counted here as 0 FLOP: conservative).  DESIGN.md §6.
 F_ALG = 60.0
-# FP64 FLOPs the kernels actually execute per ordered pair (ncu convention 2*DFMA + DMUL + DADD,
-# from the SASS loop bodies; profiles/r01/SUMMARY.md): row kernel 74, symmetric kernel 43.
-F_EXEC = {0: 74.0, 1: 43.0}
+# F_ref: FLOPs per ordered pair of the first parity-checked straightforward
+# kernel (libdevice exp/rsqrt, every ordered pair evaluated), frozen so algebraic savings show.
+F_REF = 111.0
 KERNEL_NAME = {0: "bipb::pair_kernel<MATVEC> (row kernel)", 1: "bipb::sym_kernel (symmetric-pair kernel)"}
 TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+# counter-derived FP64 FLOPs of the dominant kernel (ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}
+# of one C4 launch, 2*DFMA + DMUL + DADD; written by tools/ncu_flops.py from the committed capture)
+NCU_FLOPS_JSON = os.path.join(ROOT, "profiles", "r02", "ncu_flops.json")
+# the measured FP64 DFMA-stream peak (tools/fp64_peak.cu, best operand pattern; profiles/r02/)
+FP64_PEAK_JSON = os.path.join(ROOT, "profiles", "r02", "fp64_peak.json")
 METRIC = "fp64_pair_interactions_per_sec"
 UNIT = "pair-interactions/s"
 RESTART_M, TOL, MAX_IT = 20, 1e-10, 500
@@ -53,8 +58,12 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--precond-steps", type=int, default=None,
-                    help="extra steps with the opt-in GMRES preconditioner (reported under 'precond'; 0 = skip)")
+    ap.add_argument("--precond-steps", type=int, default=0,
+                    help="extra steps with the opt-in GMRES preconditioner (not in the paper; reported under "
+                         "'precond'; default 0 = skip)")
+    ap.add_argument("--paper-tol-steps", type=int, default=1,
+                    help="solves at the paper-like tol 1e-4 reported under 'paper_tol' (iteration context, "
+                         "PAPER.md Table 4; 0 = skip)")
     ap.add_argument("--sum", default=None, choices=["fixed", "exact"],
                     help="partial-sum mode of the symmetric product (bipb_set_sum_mode; default: the library's)")
     return ap.parse_args()
@@ -65,6 +74,23 @@ def bench_config(prob, world):
             "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
             "parallelism": f"shard x{world}, one exchange of the product per matvec" if world > 1 else "single GPU",
             "l2": "flushed between steps (256 MiB)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return ""
+
+
+def _load_json(path):
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
 
 
 def dist_env():
@@ -132,6 +158,7 @@ def oracle_sample(prob, seconds: float, cores: int):
     os.environ.setdefault("OMP_PLACES", "cores")
     import oracle
     oracle.build()
+    oracle.set_threads(cores)
     u = g.random_vector(2 * prob.n, 3)
     rows = np.linspace(0, prob.n - 1, max(cores, 16)).astype(np.int64)
     t = time.perf_counter()
@@ -162,12 +189,14 @@ def run_reference(args):
         vals.append(v)
         dts.append(dt)
     v = statistics.median(vals)
+    v1, desc1, _, _ = oracle_sample(prob, min(per_step, 6.0), 1)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(dts),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges)",
             "config": bench_config(prob, max(1, args.gpus)),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "value_1core": v1, "sample_1core": desc1, "nproc": cores, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -214,9 +243,11 @@ def run_native(args):
     def step():
         bp.bipb_source(ctx, b)
         x.zero_()
-        st, rep = bp.bipb_gmres_solve(ctx, x, None, RESTART_M, TOL, MAX_IT, check_true=False)
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, RESTART_M, tol_box[0], MAX_IT, check_true=False)
         e_box.append(bp.bipb_energy(ctx, x))
         return rep
+
+    tol_box = [TOL]
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -227,6 +258,7 @@ def run_native(args):
     ctx.timing_enable(True)
     ctx.timing_reset()
     reps, per_step_ms = [], []
+    hist_cap = MAX_IT + 1
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -273,35 +305,68 @@ def run_native(args):
         traffic = tj.get(str(kind) + ("x" if exact else ""), {}).get("bytes_per_launch")
     except Exception:
         pass
+    # counter-derived FLOPs (ncu, committed capture of the same kernel configuration at C4)
+    ncu = _load_json(NCU_FLOPS_JSON) or {}
+    ncu_k = ncu.get(f"{kind}{'x' if exact else ''}_{args.config}") or {}
+    f_exec = ncu_k.get("fp64_flops_per_ordered_pair")
+    pk = _load_json(FP64_PEAK_JSON) or {}
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "frac_basis": "F_alg-equivalent: F_alg = 60 FLOP per ORDERED pair delivered (SURVEY App. C; "
+                              "exp/rsqrt counted 0) x ordered pairs per launch / launch time; the symmetric kernel "
+                              "evaluates each unordered pair once for both rows",
                 "kernel": KERNEL_NAME[kind] + (" with exact limb sums" if exact else ""), "flops_per_unit": F_ALG,
                 "unit_of_work": "ordered matvec pair-interaction (i, j != i)",
                 "units_per_launch": pairs_per_launch, "avg_launch_ms": avg_launch_ms, "launches": mv_launches,
                 "launch_note": "one 'launch' = one operator application (all I-block groups of the symmetric kernel)",
                 "kernel_share_of_step": mv_ms / max(sum(per_step_ms), 1e-9),
-                "executed_fp64_flops_per_unit": F_EXEC[kind],
-                "executed_fp64_frac": F_EXEC[kind] * rate / 1e12 / FP64_PEAK_TFLOPS,
-                "peak_note": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (derived); measured DMUL/DADD 99.6%, "
-                             "DFMA 90% of it (tools/fp64_peak.cu)",
-                "flops_note": "F_alg = 60 FLOP/ordered pair (SURVEY App. C), exp/rsqrt counted 0"}
+                "ordered_pairs_per_s": rate,
+                "unordered_pair_evaluations_per_s": rate / 2 if kind == 1 else rate,
+                # pairs/s / (peak / F_ref), F_ref = 111 (straightforward kernel)
+                "fref_frac": rate * F_REF / 1e12 / FP64_PEAK_TFLOPS, "f_ref": F_REF,
+                # FP64 FLOPs the kernel executes (ncu counters 2*DFMA + DMUL + DADD of
+                # one launch) at this run's launch time, against the same peak
+                "executed_fp64_flops_per_unit": f_exec,
+                "ncu_fp64_flop_frac": (f_exec * rate / 1e12 / FP64_PEAK_TFLOPS) if f_exec else None,
+                "ncu_fp64_flop_frac_at_capture": ncu_k.get("ncu_fp64_flop_frac"),
+                "ncu_fp64_pipe_active": ncu_k.get("fp64_pipe_active_pct"),
+                "ncu_source": ncu_k.get("source"),
+                "peak_measured": pk.get("best_dfma_tflops"), "peak_measured_source": pk.get("source"),
+                "peak_note": "peak = 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (unit counts x clock, the ncu "
+                             "FP64 roofline's 2 x DFMA peak; MEASURED_PEAKS.json has no FP64 entry); "
+                             "peak_measured = best DFMA stream measured on the box (tools/fp64_peak.cu)"}
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere + uniform charges, bipb_inputs)",
-            "config": dict(bench_config(prob, world), exchange=ctx.exchange,
-                           sums=("exact fixed-point limbs" if exact else "fixed-order double partials")
-                           if kind == 1 else "fixed-order chunk partials"),
+            "config": bench_config(prob, world),
+            "exchange": ctx.exchange,
+            "sums": ("exact fixed-point limbs" if exact else "fixed-order double partials")
+            if kind == 1 else "fixed-order chunk partials",
+            "cuda_graphs": os.environ.get("BIPB_GRAPHS") == "1",
+            "input_sha256": prob.sha256(),
+            "residual_history": [float(h) for h in reps[-1]["history"]],
             "time_to_solution_s": total_ms / args.steps / 1e3,
             "iterations": [r["iterations"] for r in reps], "matvecs": matvecs,
             "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),
             "kernel_ms": {"matvec": mv_ms, "source": src_ms, "energy": en_ms, "steps_sum": sum(per_step_ms)},
             "roofline": roofline, "clocks": clocks}
 
+    # ---- paper-like tolerance ("one tol = 1e-4 run per config"; Table 4 N_it 9-11)
+    if args.paper_tol_steps > 0:
+        tol_box[0] = 1e-4
+        preps = [step() for _ in range(args.paper_tol_steps)]
+        tol_box[0] = TOL
+        line["paper_tol"] = {"tol": 1e-4, "iterations": [r["iterations"] for r in preps],
+                             "energy_kcal_mol": e_box[-1],
+                             "energy_rel_diff_vs_tol_1e-10": abs(e_box[-1] / line["energy_kcal_mol"] - 1.0),
+                             "note": "iteration context only (PAPER.md Table 4 reports 9-11 at its unstated "
+                                     "tolerance); not timed into value"}
+
     # ---- the same step with the opt-in right preconditioner (bipb_set_precond: jump-term diagonal;
     # NOT the paper's plain GMRES, so reported beside the headline, not in it)
-    kp = args.precond_steps if args.precond_steps is not None else min(args.steps, 2)
+    kp = args.precond_steps
     if kp > 0:
         ctx.set_precond(1)
         e_plain = e_box[-1]
@@ -384,7 +449,9 @@ def run_native(args):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         v, desc, _, _ = oracle_sample(prob, args.cpu_seconds, cores)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        v1, desc1, _, _ = oracle_sample(prob, min(args.cpu_seconds, 6.0), 1)  # the paper's "one CPU" framing
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                                "value_1core": v1, "sample_1core": desc1, "nproc": cores, "cpu_model": cpu_model()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

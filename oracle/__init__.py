@@ -46,6 +46,7 @@ def lib():
         L = ctypes.CDLL(_LIB)
         d, i, p = ctypes.c_double, _I, _D
         for name, args, res in [
+            ("orc_set_threads", [i], None), ("orc_get_threads", [], i),
             ("orc_G0", [p, p], d), ("orc_Gk", [p, p, d], d),
             ("orc_dG0_dny", [p, p, p], d), ("orc_dGk_dny", [p, p, p, d], d),
             ("orc_dG0_dnx", [p, p, p], d), ("orc_dGk_dnx", [p, p, p, d], d),
@@ -76,6 +77,15 @@ def _p(a):
 
 def _c(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of later oracle calls (timing only; results do not depend on it)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
 
 
 def eps_ratio(eps1: float, eps2: float) -> float:

@@ -29,11 +29,18 @@
  * identity and the 2x2 example of SPEC.md S:183, GMRES vs LAPACK on the dense A.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 #define ORC_PI 3.14159265358979323846
+
+/* OpenMP threads of the following calls (timing legs: bench.py times the oracle on all host cores
+ * and on one, the paper's "one CPU" framing).  No effect on any result: every parallel
+ * loop is over independent rows with a fixed per-row order. */
+void orc_set_threads(int64_t n) { omp_set_num_threads((int)(n > 0 ? n : 1)); }
+int64_t orc_get_threads(void) { return (int64_t)omp_get_max_threads(); }
 
 /* ---------------------------------------------------------------- vector helpers */
 static double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }

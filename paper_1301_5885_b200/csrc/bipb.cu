@@ -3,6 +3,7 @@
 // row-sharded exchange.  Paper: Geng & Jacob, arXiv 1301.5885 (Table 1).
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -77,6 +78,13 @@ static_assert((SymCfgMid::TPB * SymCfgMid::T) % TILE == 0, "symmetric block must
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
 constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
 constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
+
+// NVTX ranges per phase (SURVEY.md §5 "tracing"): visible in nsys / ncu --nvtx timelines; a no-op
+// when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 static bipb_status fail(bipb_status st, const std::string& msg) {
@@ -1211,6 +1219,7 @@ bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const
                        const double* areas, int64_t nc, const double* charges, double eps1, double eps2,
                        double kappa, const bipb_dist* dist, void* cuda_stream) {
   g_err.clear();
+  NvtxRange nvtx_("bipb_setup");
   if (!out) return fail(BIPB_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (n < 1) return fail(BIPB_ERR_ARG, "n must be >= 1");
@@ -1234,6 +1243,7 @@ bipb_status bipb_setup(bipb_ctx** out, int64_t n, const double* centroids, const
 }
 
 bipb_status bipb_source(bipb_ctx* c, double* b) {
+  NvtxRange nvtx_("bipb_source");
   if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");
   CKS(check_alive(c));
   const int64_t n = c->n;
@@ -1273,6 +1283,7 @@ bipb_status bipb_source(bipb_ctx* c, double* b) {
 }
 
 bipb_status bipb_matvec(bipb_ctx* c, const double* u, double* y) {
+  NvtxRange nvtx_("bipb_matvec");
   if (!c || !u || !y) return fail(BIPB_ERR_ARG, "NULL argument");
   CKS(check_alive(c));
   if (u == y) return fail(BIPB_ERR_ARG, "u and y must not alias");
@@ -1387,6 +1398,7 @@ static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
 // Run step k: replay its CUDA graph when possible (no timing instrumentation active, the
 // product's buffers warm), else enqueue eagerly; then wait and return (rel, h_{k+1,k}).
 static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
+  NvtxRange nvtx_("arnoldi_step");
   // opt-in (BIPB_GRAPHS=1): replay pays off only from the second solve in a context (measured:
   // C1 3.25 -> 2.82 ms per solve, C2 -2.6%, C3/C4 within noise; the first solve pays the capture)
   static const bool graphs_on = getenv("BIPB_GRAPHS") && !strcmp(getenv("BIPB_GRAPHS"), "1");
@@ -1626,6 +1638,7 @@ static bipb_status gmres_batch_impl(bipb_ctx* c, int R, const double* const* bd,
 
 bipb_status bipb_gmres_solve(bipb_ctx* c, const double* b, double* x, int32_t restart_m, double tol,
                              int32_t max_iters, int32_t check_true, bipb_report* rep) {
+  NvtxRange nvtx_("bipb_gmres_solve");
   if (!c || !x) return fail(BIPB_ERR_ARG, "NULL argument");
   if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
   CKS(check_alive(c));
@@ -1748,6 +1761,7 @@ rerun:
 
 bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, double* X, int32_t restart_m,
                                    double tol, int32_t max_iters, int32_t check_true, bipb_report* reps) {
+  NvtxRange nvtx_("bipb_gmres_solve_batch");
   if (!c || !B || !X || nrhs < 1) return fail(BIPB_ERR_ARG, "NULL argument or nrhs < 1");
   CKS(check_alive(c));
   if (restart_m < 1 || max_iters < 1 || !(tol > 0)) return fail(BIPB_ERR_ARG, "restart_m, max_iters >= 1, tol > 0");
@@ -1785,6 +1799,7 @@ bipb_status bipb_gmres_solve_batch(bipb_ctx* c, int32_t nrhs, const double* B, d
 }
 
 bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi_reac) {
+  NvtxRange nvtx_("bipb_energy");
   if (!c || !x || !e_sol) return fail(BIPB_ERR_ARG, "NULL argument");
   CKS(check_alive(c));
   const int64_t n = c->n, nc = c->nc, m2 = 2 * n;
@@ -1840,6 +1855,7 @@ bipb_status bipb_energy(bipb_ctx* c, const double* x, double* e_sol, double* phi
 }
 
 bipb_status bipb_matvec_batch(bipb_ctx* c, int32_t nrhs, const double* U, double* Y) {
+  NvtxRange nvtx_("bipb_matvec_batch");
   if (!c || !U || !Y || nrhs < 1) return fail(BIPB_ERR_ARG, "bad argument");
   CKS(check_alive(c));
   const int64_t m2 = 2 * c->n;

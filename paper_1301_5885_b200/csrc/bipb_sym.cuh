@@ -29,6 +29,13 @@ namespace bipb {
 #ifndef BIPB_SYM_PREFETCH
 #define BIPB_SYM_PREFETCH 1
 #endif
+// unroll factor of the 32-step source rotation (tuning: > 1 lets the compiler overlap one step's
+// reverse-accumulator chain + shuffles with the next step's independent work)
+#ifndef BIPB_SYM_STUNROLL
+#define BIPB_SYM_STUNROLL 1
+#endif
+#define BIPB_PRAGMA_(x) _Pragma(#x)
+#define BIPB_UNROLL_(n) BIPB_PRAGMA_(unroll n)
 // tuning variants of the per-step reverse accumulation (see the main loop); 0 = one chain
 #ifndef BIPB_SYM_RVSPLIT
 #define BIPB_SYM_RVSPLIT 0
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
         // the next step's record is loaded while this step computes (software pipelining)
         SymSrc<R> nxt;
         rec_load<R>(sb, g0 + lane, nxt);
-#pragma unroll 1
+        BIPB_UNROLL_(BIPB_SYM_STUNROLL)
         for (int st = 0; st < 32; ++st) {
           const SymSrc<R> sj = nxt;
           rec_load<R>(sb, g0 + ((lane + st + 1) & 31), nxt);  // wraps harmlessly at st = 31

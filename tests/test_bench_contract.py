@@ -26,14 +26,26 @@ def test_reference_arm_json():
     assert REQUIRED <= set(d) and d["impl"] == "reference"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0 and d["gpu_launches"] == 0
+    cb = d["cpu_baseline"]  # all host cores and one core (the paper's "one CPU"), with the CPU model
+    assert cb["value_1core"] > 0 and cb["nproc"] >= 1 and "cpu_model" in cb
+    # identical config keys in both arms (the driver compares them)
+    sys.path.insert(0, ROOT)
+    import bench
+    import bipb_inputs as g
+    assert d["config"] == json.loads(json.dumps(bench.bench_config(g.config("C1"), 1)))
 
 
 @pytest.mark.gpu
 def test_native_arm_json():
-    d = _run(["--config", "C2", "--steps", "1", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "2"], 900)
+    d = _run(["--config", "C2", "--steps", "1", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "2",
+              "--precond-steps", "1"], 900)
     assert REQUIRED <= set(d) and d["metric"] == "fp64_pair_interactions_per_sec"
     r = d["roofline"]
     assert r["bound"] == "alu" and 0 < r["frac"] < 1.5 and r["peak"] > 30
+    assert {"fref_frac", "ncu_fp64_flop_frac", "executed_fp64_flops_per_unit", "peak_measured",
+            "unordered_pair_evaluations_per_s"} <= set(r)
+    assert d["paper_tol"]["tol"] == 1e-4 and max(d["paper_tol"]["iterations"]) < min(d["iterations"])
+    assert len(d["input_sha256"]) == 64 and len(d["residual_history"]) == d["iterations"][-1]
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["cpu_baseline"]["kind"] == "oracle"
@@ -56,4 +68,4 @@ def test_native_arm_two_ranks_one_gpu():
     assert len(lines) == 1  # rank 0 only
     d = json.loads(lines[0])
     assert REQUIRED <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "strong" and "cpu_baseline" not in d
-    assert d["config"]["exchange"] == "p2p"  # default: peer stores (both ranks map each other's mailbox)
+    assert d["exchange"] == "p2p"  # default: peer stores (both ranks map each other's mailbox)

@@ -27,6 +27,8 @@ for w in $WHAT; do
       ncu -i /tmp/prof_sym_$TAG.ncu-rep --page source --csv --print-source sass > $O/prof_sym_sass.csv 2>&1
       ncu -i /tmp/prof_sym_$TAG.ncu-rep --page details --csv > $O/prof_sym_details.csv 2>&1
       ls -la $O ;;
+    tune)
+      python tools/tune_matvec.py run C4 3 > $O/tune_sym_C4.jsonl 2> $O/tune_sym_C4.err; cat $O/tune_sym_C4.jsonl ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
         python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --precond-steps 0 > /dev/null 2>&1 ;;

@@ -17,10 +17,13 @@ VARIANTS = []
 # extra -D macros ("defs")
 # (session 2: {"BIPB_RSQ_INT": 1}, {"BIPB_EXP_F32K": 1} and both measured slower at C4 —
 # profiles/r01/tune_int_variants_C4.jsonl; now: block-shape sweep for mid-size problems)
-# (block-shape sweep for R = 1: profiles/r01/tune_shape_C*.jsonl); multi-RHS shapes (`batch` mode):
-for t2, t4 in ((2, 2), (4, 3), (3, 3), (4, 2)):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM2_T": t2, "BIPB_SYM4_T": t4}})
+# (block-shape sweep for R = 1: profiles/r01/tune_shape_C*.jsonl); multi-RHS shapes (`batch` mode,
+# profiles/r01/tune_batch_shapes_C4.jsonl).
+# r02: R = 1 issue-efficiency set at C4: unrolling the 32-step source rotation
+# (overlap of one step's reverse-accumulator chain with the next step) at T = 5 / 4, and occupancy.
+for t, minb, un in ((5, 1, 1), (5, 1, 2), (4, 1, 2), (4, 2, 1), (4, 2, 2), (3, 3, 2)):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
+                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM_STUNROLL": un}})
 
 
 def name(v):
