@@ -54,8 +54,13 @@ struct SymLayout {
   __host__ __device__ static constexpr int C(int r) { return (R == 1) ? 3 : 6 + 2 * r; }
   __host__ __device__ static constexpr int A(int r) { return (R == 1) ? 4 : 7 + 2 * r; }
 };
-// source rows per warp-combine of the reverse sums (see sym_kernel)
-__host__ __device__ constexpr int sym_rs_rows(int R, int B) { return R == 1 ? B : TILE; }
+// source rows per warp-combine of the reverse sums (see sym_kernel): the whole J-block for R = 1
+// (one barrier per J-block), every stage for R > 1 -- or for R = 1 too with BIPB_SYM_RS_STAGE=1,
+// which cuts the shared memory of a T = 5 CTA from ~82 KB to ~49 KB (3 CTAs per SM fit)
+#ifndef BIPB_SYM_RS_STAGE
+#define BIPB_SYM_RS_STAGE 0
+#endif
+__host__ __device__ constexpr int sym_rs_rows(int R, int B) { return (R == 1 && !BIPB_SYM_RS_STAGE) ? B : TILE; }
 __host__ __device__ constexpr int64_t sym_idx(int64_t j, int f, int F) {
   return (j / TILE) * (TILE * F) + f * TILE + (j % TILE);
 }

@@ -11,7 +11,7 @@ mkdir -p $O
 for w in $WHAT; do
   case $w in
     tests)
-      OMP_NUM_THREADS=${PAYLOAD_OMP:-4} timeout ${TEST_TIMEOUT:-2700} python -m pytest tests -m gpu -q -p no:cacheprovider \
+      OMP_NUM_THREADS=${PAYLOAD_OMP:-4} timeout ${TEST_TIMEOUT:-2300} python -m pytest tests -m gpu -q -p no:cacheprovider \
         --timeout 1200 -rfEs > $O/pytest_gpu.txt 2>&1
       tail -30 $O/pytest_gpu.txt ;;
     peak)

@@ -21,9 +21,12 @@ VARIANTS = []
 # profiles/r01/tune_batch_shapes_C4.jsonl).
 # r02: R = 1 issue-efficiency set at C4: unrolling the 32-step source rotation
 # (overlap of one step's reverse-accumulator chain with the next step) at T = 5 / 4, and occupancy.
-for t, minb, un in ((5, 1, 1), (5, 1, 2), (4, 1, 2), (4, 2, 1), (4, 2, 2), (3, 3, 2)):
+# 3 CTAs per SM (12 warps, 3 per scheduler) at T = 4 / 5: 166 registers without spills; T = 5 needs
+# the per-stage combine of the reverse sums (BIPB_SYM_RS_STAGE) to fit 3 x 49 KB of shared memory.
+for t, minb, un, rs in ((5, 1, 1, 0), (5, 1, 2, 0), (4, 1, 2, 0), (4, 2, 1, 0), (3, 3, 2, 0),
+                        (5, 1, 1, 1), (5, 3, 1, 1), (5, 3, 2, 1), (4, 3, 1, 0), (4, 3, 2, 0), (4, 3, 1, 1)):
     VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM_STUNROLL": un}})
+                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM_STUNROLL": un, "BIPB_SYM_RS_STAGE": rs}})
 
 
 def name(v):
