@@ -369,7 +369,7 @@ def run_native(args):
     kp = args.precond_steps
     if kp > 0:
         ctx.set_precond(1)
-        e_plain = e_box[-1]
+        e_plain = line["energy_kcal_mol"]  # the headline solve's (tol 1e-10), not the paper_tol leg's
         flush.zero_()
         step()  # warm-up (graph capture if enabled)
         torch.cuda.synchronize()

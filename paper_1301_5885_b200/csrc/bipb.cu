@@ -1025,9 +1025,9 @@ static bipb_status p2p_setup(bipb_ctx* c, bool require) {
         if (atoi(pf) == c->rank && why.empty()) why = "probe failure forced (BIPB_P2P_PROBE_FAIL)";
       CKS(agree(why.empty(), &all_ok));
     }
-    dfree(c, dsend);
-    dfree(c, drecv);
     if (!all_ok) {
+      dfree(c, dsend);
+      dfree(c, drecv);
       p2p_teardown(c);
       if (require)
         return fail(BIPB_ERR_NCCL, "BIPB_DIST_P2P: peer-store exchange unavailable" +
@@ -1041,6 +1041,8 @@ static bipb_status p2p_setup(bipb_ctx* c, bool require) {
     double dummy = 0.0;
     std::vector<double> bar((size_t)c->world);
     CKS(allgather(&dummy, 1, bar.data()));
+    dfree(c, dsend);
+    dfree(c, drecv);
   }
   CK(cudaStreamSynchronize(c->stream));
   c->p2p = true;

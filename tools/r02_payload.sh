@@ -11,9 +11,11 @@ mkdir -p $O
 for w in $WHAT; do
   case $w in
     tests)
-      OMP_NUM_THREADS=${PAYLOAD_OMP:-4} timeout ${TEST_TIMEOUT:-2300} python -m pytest tests -m gpu -q -p no:cacheprovider \
-        --timeout 1200 -rfEs > $O/pytest_gpu.txt 2>&1
+      OMP_NUM_THREADS=${PAYLOAD_OMP:-4} timeout ${TEST_TIMEOUT:-2300} python -m pytest ${PYTEST_SEL:-tests} -m gpu -q \
+        -p no:cacheprovider --timeout 1200 -rfEs > $O/pytest_gpu.txt 2>&1
       tail -30 $O/pytest_gpu.txt ;;
+    smoke)
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -3 $O/smoke.txt ;;
     peak)
       tools/fp64_peak > $O/fp64_peak.jsonl 2>&1; tools/dmma_probe > $O/dmma_probe.jsonl 2>&1 ;;
     bench)

@@ -22,9 +22,11 @@ VARIANTS = []
 # r02: R = 1 issue-efficiency set at C4: unrolling the 32-step source rotation
 # (overlap of one step's reverse-accumulator chain with the next step) at T = 5 / 4, and occupancy.
 # 3 CTAs per SM (12 warps, 3 per scheduler) at T = 4 / 5: 166 registers without spills; T = 5 needs
-# the per-stage combine of the reverse sums (BIPB_SYM_RS_STAGE) to fit 3 x 49 KB of shared memory.
+# the per-stage combine of the reverse sums (BIPB_SYM_RS_STAGE) to fit 3 x 49 KB of shared memory;
+# 4 CTAs per SM: T = 3 at 128 registers (no spills), T = 4 (small spills).
 for t, minb, un, rs in ((5, 1, 1, 0), (5, 1, 2, 0), (4, 1, 2, 0), (4, 2, 1, 0), (3, 3, 2, 0),
-                        (5, 1, 1, 1), (5, 3, 1, 1), (5, 3, 2, 1), (4, 3, 1, 0), (4, 3, 2, 0), (4, 3, 1, 1)):
+                        (5, 1, 1, 1), (5, 3, 1, 1), (5, 3, 2, 1), (4, 3, 1, 0), (4, 3, 2, 0), (4, 3, 1, 1),
+                        (3, 4, 1, 1), (3, 4, 2, 1), (4, 4, 1, 1)):
     VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
                      "tile": 128, "stages": 3, "defs": {"BIPB_SYM_STUNROLL": un, "BIPB_SYM_RS_STAGE": rs}})
 
