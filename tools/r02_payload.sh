@@ -31,6 +31,18 @@ for w in $WHAT; do
       ls -la $O ;;
     tune)
       python tools/tune_matvec.py run C4 3 > $O/tune_sym_C4.jsonl 2> $O/tune_sym_C4.err; cat $O/tune_sym_C4.jsonl ;;
+    sanitize)
+      for t in memcheck racecheck synccheck initcheck; do
+        timeout 900 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_driver.py > $O/sanitize_$t.txt 2>&1
+        tail -3 $O/sanitize_$t.txt
+      done ;;
+    configs)
+      for c in C1 C2 C3; do
+        timeout 600 python bench.py --config $c --e2e-steps 0 --no-cpu-baseline --paper-tol-steps 1 > $O/bench_$c.json 2> $O/bench_$c.err
+        tail -c 400 $O/bench_$c.json
+      done ;;
+    shards)
+      timeout 900 python tools/shard_scaling.py C4 > $O/shard_scaling_C4.jsonl 2>&1; cat $O/shard_scaling_C4.jsonl ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
         python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --precond-steps 0 > /dev/null 2>&1 ;;

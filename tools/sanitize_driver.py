@@ -26,4 +26,11 @@ for kappa in (g.KAPPA, 0.0):
             sol = bp.solve(ctx, restart_m=10, tol=1e-8)
             sol = bp.solve(ctx, restart_m=10, tol=1e-8, precond=1)
         ctx.close()
+# r02: an eps1 != 1, large-kappa case (edge parameters) and the exact-sum symmetric product
+pe = g.sphere_problem(3, 4.0, g.charges_in_ball(11, 3.0, 1), eps1=2.0, eps2=80.0, kappa=2.0)
+ctx = bp.bipb_setup(pe.centroids, pe.normals, pe.areas, pe.charges, pe.eps1, pe.eps2, pe.kappa)
+ctx.set_matvec_kernel(1)
+ctx.set_sum_mode(1)
+bp.solve(ctx, restart_m=20, tol=1e-10)
+ctx.close()
 print("sanitize driver done")
