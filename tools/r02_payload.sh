@@ -30,7 +30,8 @@ for w in $WHAT; do
       ncu -i /tmp/prof_sym_$TAG.ncu-rep --page details --csv > $O/prof_sym_details.csv 2>&1
       ls -la $O ;;
     tune)
-      python tools/tune_matvec.py run C4 3 > $O/tune_sym_C4.jsonl 2> $O/tune_sym_C4.err; cat $O/tune_sym_C4.jsonl ;;
+      python tools/tune_matvec.py run C4 3 > $O/tune_sym_C4.jsonl 2> $O/tune_sym_C4.err; cat $O/tune_sym_C4.jsonl
+      python tools/tune_matvec.py runbatch C4 > $O/tune_batch_C4.jsonl 2> $O/tune_batch_C4.err; cat $O/tune_batch_C4.jsonl ;;
     sanitize)
       for t in memcheck racecheck synccheck initcheck; do
         timeout 900 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_driver.py > $O/sanitize_$t.txt 2>&1

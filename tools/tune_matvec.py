@@ -23,12 +23,17 @@ VARIANTS = []
 # (overlap of one step's reverse-accumulator chain with the next step) at T = 5 / 4, and occupancy.
 # 3 CTAs per SM (12 warps, 3 per scheduler) at T = 4 / 5: 166 registers without spills; T = 5 needs
 # the per-stage combine of the reverse sums (BIPB_SYM_RS_STAGE) to fit 3 x 49 KB of shared memory;
-# 4 CTAs per SM: T = 3 at 128 registers (no spills), T = 4 (small spills).
-for t, minb, un, rs in ((5, 1, 1, 0), (5, 1, 2, 0), (4, 1, 2, 0), (4, 2, 1, 0), (3, 3, 2, 0),
-                        (5, 1, 1, 1), (5, 3, 1, 1), (5, 3, 2, 1), (4, 3, 1, 0), (4, 3, 2, 0), (4, 3, 1, 1),
-                        (3, 4, 1, 1), (3, 4, 2, 1), (4, 4, 1, 1)):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3, "defs": {"BIPB_SYM_STUNROLL": un, "BIPB_SYM_RS_STAGE": rs}})
+# 4 CTAs per SM: T = 3 at 128 registers (no spills), T = 4 (small spills).  All slower (session 1,
+# profiles/r02/tune_sym_C4.jsonl).  Session 3: the non-FP64 instructions of a step (the prefetched
+# record's register moves: ping-pong buffers, PREFETCH = 2; the exp exponent clamp: NOCLAMP is a
+# speed probe only, exact at C4 which has no padded rows), and the baseline twice for the noise.
+# The multi-RHS kernels (R = 2, 4) spend ~16 register moves per pair on the prefetched record copy
+# (40 IMAD.MOV per R = 4 step): PREFETCH = 0 / 2 are timed for them too (`runbatch`).
+for t, minb, un, rs, pf, nc in ((5, 1, 1, 0, 1, 0), (5, 1, 1, 0, 2, 0), (5, 1, 1, 0, 1, 1), (5, 1, 1, 1, 1, 0),
+                                (5, 1, 1, 0, 2, 1), (5, 1, 1, 0, 0, 0), (5, 1, 1, 0, 1, 0)):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": pf, "un": 1,
+                     "tile": 128, "stages": 3,
+                     "defs": {"BIPB_SYM_STUNROLL": un, "BIPB_SYM_RS_STAGE": rs, "BIPB_EXP_NOCLAMP": nc}})
 
 
 def name(v):
@@ -140,7 +145,7 @@ if __name__ == "__main__":
                                  timeout=900)
             for line in out.stdout.strip().splitlines():
                 d = json.loads(line)
-                d.update(v["defs"])
+                d.update({"pf": v.get("pf"), **v["defs"]})
                 print(json.dumps(d), flush=True)
             if out.returncode:
                 print(json.dumps({"error": out.stderr[-400:], **v["defs"]}), flush=True)
