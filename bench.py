@@ -37,7 +37,7 @@ F_ALG = 60.0
 # kernel (libdevice exp/rsqrt, every ordered pair evaluated), frozen so algebraic savings show.
 F_REF = 111.0
 KERNEL_NAME = {0: "bipb::pair_kernel<MATVEC> (row kernel)", 1: "bipb::sym_kernel (symmetric-pair kernel)"}
-TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r02", "traffic.json")
 # counter-derived FP64 FLOPs of the dominant kernel (ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}
 # of one C4 launch, 2*DFMA + DMUL + DADD; written by tools/ncu_flops.py from the committed capture)
 NCU_FLOPS_JSON = os.path.join(ROOT, "profiles", "r02", "ncu_flops.json")

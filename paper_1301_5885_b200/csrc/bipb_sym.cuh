@@ -36,10 +36,13 @@ namespace bipb {
 #endif
 #define BIPB_PRAGMA_(x) _Pragma(#x)
 #define BIPB_UNROLL_(n) BIPB_PRAGMA_(unroll n)
-// tuning variants of the per-step reverse accumulation (see the main loop); 0 = one chain
-#ifndef BIPB_SYM_RVSPLIT
-#define BIPB_SYM_RVSPLIT 0
+// record prefetch of the 32-step rotation, per number of operands: 1 = load the next step's
+// record while this one computes (register copy per step), 2 = ping-pong buffers (no copies, two
+// records live), 0 = load at the top of each step (no copies, load latency exposed)
+#ifndef BIPB_SYM_PREFETCH_MRHS
+#define BIPB_SYM_PREFETCH_MRHS BIPB_SYM_PREFETCH
 #endif
+__host__ __device__ constexpr int sym_prefetch(int R) { return R == 1 ? BIPB_SYM_PREFETCH : BIPB_SYM_PREFETCH_MRHS; }
 
 // Record (tile-SoA): fields x, y, z (scaled by s), nx, ny, nz, then (c_r, a'_r) for r < R with
 // c = W u_dphi and a' = s W u_phi.  For every TILE-source tile the F = 6 + 2R fields are
@@ -289,76 +292,9 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
       Acc2 rv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) rv[r].p0 = rv[r].p1 = 0.0;
-#if BIPB_SYM_RVSPLIT == 1
-      Acc2 rv2[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) rv2[r].p0 = rv2[r].p1 = 0.0;
-#endif
       if (o != 0 && gcnt == 32) {
-#if BIPB_SYM_PREFETCH == 2
-        // ping-pong record buffers: the next step's record loads while this step computes, with
-        // no register copies between steps (loop unrolled by two)
-        SymSrc<R> ra, rb;
-        rec_load<R>(sb, g0 + lane, ra);
-#pragma unroll 1
-        for (int st = 0; st < 32; st += 2) {
-          rec_load<R>(sb, g0 + ((lane + st + 1) & 31), rb);
-#pragma unroll
-          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], ra, kc, s_tab, fa[k], rv);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
-            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
-          }
-          rec_load<R>(sb, g0 + ((lane + st + 2) & 31), ra);  // wraps harmlessly at st = 30
-#pragma unroll
-          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], rb, kc, s_tab, fa[k], rv);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
-            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
-          }
-        }
-#else
-#if BIPB_SYM_PREFETCH
-        // the next step's record is loaded while this step computes (software pipelining)
-        SymSrc<R> nxt;
-        rec_load<R>(sb, g0 + lane, nxt);
-        BIPB_UNROLL_(BIPB_SYM_STUNROLL)
-        for (int st = 0; st < 32; ++st) {
-          const SymSrc<R> sj = nxt;
-          rec_load<R>(sb, g0 + ((lane + st + 1) & 31), nxt);  // wraps harmlessly at st = 31
-#else
-#pragma unroll 1
-        for (int st = 0; st < 32; ++st) {
-          SymSrc<R> sj;
-          rec_load<R>(sb, g0 + ((lane + st) & 31), sj);
-#endif
-#if BIPB_SYM_RVSPLIT == 1
-          // two rotating accumulator sets (even / odd targets): halves the dependent FMA chain
-          // that ends each step, at the price of a second set of shuffles
-#pragma unroll
-          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], (k & 1) ? rv2 : rv);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
-            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
-            rv2[r].p0 = __shfl_sync(0xffffffffu, rv2[r].p0, (lane + 1) & 31);
-            rv2[r].p1 = __shfl_sync(0xffffffffu, rv2[r].p1, (lane + 1) & 31);
-          }
-#elif BIPB_SYM_RVSPLIT == 2
-          // odd targets into a fresh per-step accumulator, added once (one DADD per quantity)
-          Acc2 st2[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) st2[r].p0 = st2[r].p1 = 0.0;
-#pragma unroll
-          for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], (k & 1) ? st2 : rv);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0 + st2[r].p0, (lane + 1) & 31);
-            rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1 + st2[r].p1, (lane + 1) & 31);
-          }
-#else
+        // one step: the T targets against source sj, then the reverse accumulators move one lane
+        auto step = [&](const SymSrc<R>& sj) {
 #pragma unroll
           for (int k = 0; k < T; ++k) pair_sym<SCREENED, R>(tg[k], sj, kc, s_tab, fa[k], rv);
 #pragma unroll
@@ -366,16 +302,38 @@ __global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
             rv[r].p0 = __shfl_sync(0xffffffffu, rv[r].p0, (lane + 1) & 31);
             rv[r].p1 = __shfl_sync(0xffffffffu, rv[r].p1, (lane + 1) & 31);
           }
-#endif
+        };
+        constexpr int PF = sym_prefetch(R);
+        if constexpr (PF == 2) {
+          // ping-pong record buffers: the next step's record loads while this step computes, with
+          // no register copies between steps (loop unrolled by two)
+          SymSrc<R> ra, rb;
+          rec_load<R>(sb, g0 + lane, ra);
+#pragma unroll 1
+          for (int st = 0; st < 32; st += 2) {
+            rec_load<R>(sb, g0 + ((lane + st + 1) & 31), rb);
+            step(ra);
+            rec_load<R>(sb, g0 + ((lane + st + 2) & 31), ra);  // wraps harmlessly at st = 30
+            step(rb);
+          }
+        } else if constexpr (PF == 1) {
+          // the next step's record is loaded while this step computes (software pipelining)
+          SymSrc<R> nxt;
+          rec_load<R>(sb, g0 + lane, nxt);
+          BIPB_UNROLL_(BIPB_SYM_STUNROLL)
+          for (int st = 0; st < 32; ++st) {
+            const SymSrc<R> sj = nxt;
+            rec_load<R>(sb, g0 + ((lane + st + 1) & 31), nxt);  // wraps harmlessly at st = 31
+            step(sj);
+          }
+        } else {
+#pragma unroll 1
+          for (int st = 0; st < 32; ++st) {
+            SymSrc<R> sj;
+            rec_load<R>(sb, g0 + ((lane + st) & 31), sj);
+            step(sj);
+          }
         }
-#if BIPB_SYM_RVSPLIT == 1
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          rv[r].p0 += rv2[r].p0;
-          rv[r].p1 += rv2[r].p1;
-        }
-#endif
-#endif
       } else {
         // diagonal block (pairs i < j only) or a partial group
 #pragma unroll 1
