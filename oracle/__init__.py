@@ -23,7 +23,9 @@ CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-s
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+        tmp = f"{_LIB}.{os.getpid()}.tmp"  # renamed into place: a running process keeps its mapping
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 
@@ -236,6 +238,10 @@ def gmres_checkpointed(prob, b, store, restart=20, tol=1e-10, max_iters=500, che
         xv = np.ctypeslib.as_array(xp, (m,))
         yv = np.ctypeslib.as_array(yp, (m,))
         h = hashlib.sha256(xv.tobytes()).hexdigest()[:16]
+        if k not in have:  # a product another process stored meanwhile (merged from a GPU-box run)
+            for f in os.listdir(store):
+                if f.startswith(f"{k:03d}_") and f.endswith(".npy"):
+                    have[k] = (f[4:-4], os.path.join(store, f))
         if k in have:
             if have[k][0] != h:
                 err.append(f"stored product {k} was made from another x ({have[k][0]} vs {h})")

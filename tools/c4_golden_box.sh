@@ -9,7 +9,7 @@ set -u
 LIMIT=${1:-3300}; shift || true
 STORE=/tmp/bipb_c4_store
 mkdir -p gpurun_out/c4_store $STORE/C4_m20
-[ -d tools/c4_store ] && cp -n tools/c4_store/*.npy $STORE/C4_m20/ 2>/dev/null
+[ -d tools/c4_store/C4_m20 ] && cp -n tools/c4_store/C4_m20/*.npy $STORE/C4_m20/ 2>/dev/null
 ls $STORE/C4_m20 > /tmp/c4_before.txt
 lscpu > gpurun_out/c4_golden_lscpu.txt
 python -c "import oracle; oracle.build(force=True)"
