@@ -121,6 +121,7 @@ def test_solve_parity_golden(bp, cfg):
     for m, ref in gold["solves"].items():
         rows = np.array(ref["rows"])
         np.testing.assert_allclose(b[rows], ref["b_phi"], rtol=1e-12, atol=1e-14 * ref["b_norm"])
+        np.testing.assert_allclose(b[rows + p.n], ref["b_dphi"], rtol=1e-12, atol=1e-14 * ref["b_norm"])
         x = np.zeros(2 * p.n)
         st, rep = bp.bipb_gmres_solve(ctx, x, None, int(m), gold["tol"], 500, check_true=True)
         e = bp.bipb_energy(ctx, x)
@@ -128,6 +129,7 @@ def test_solve_parity_golden(bp, cfg):
         assert abs(rep["iterations"] - ref["iterations"]) <= 1
         assert e == pytest.approx(ref["energy"], rel=1e-8)
         np.testing.assert_allclose(x[rows], ref["x_phi"], rtol=1e-7, atol=1e-9 * ref["x_norm"])
+        np.testing.assert_allclose(x[rows + p.n], ref["x_dphi"], rtol=1e-7, atol=1e-9 * ref["x_norm"])
     ctx.close()
 
 
