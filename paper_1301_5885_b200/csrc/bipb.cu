@@ -76,7 +76,13 @@ constexpr int64_t SYM_SMALL_TASKS = 2048;
 static_assert((SymCfg<1>::TPB * SymCfg<1>::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 static_assert((SymCfgMid::TPB * SymCfgMid::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
-constexpr int EN_TPB = 128, EN_T = 2, EN_MINB = 4;
+#ifndef BIPB_EN_T
+#define BIPB_EN_T 4  // r02 A/B (profiles/r02/session4/tune_energy_C*.jsonl): C4 3.69 -> 3.40 ms with the wave rule
+#endif
+#ifndef BIPB_EN_MINB
+#define BIPB_EN_MINB 2
+#endif
+constexpr int EN_TPB = 128, EN_T = BIPB_EN_T, EN_MINB = BIPB_EN_MINB;
 constexpr int64_t WANT_CTAS = 148 * 16;  // enough CTAs for a short dynamic-scheduling tail
 
 // NVTX ranges per phase (SURVEY.md §5 "tracing"): visible in nsys / ncu --nvtx timelines; a no-op
@@ -221,6 +227,7 @@ struct bipb_ctx {
   double* bat_U = nullptr;  // [4][2n] batch staging (host inputs)
   double* bat_Y = nullptr;
   int64_t chunk_mv = 0, nchunk_mv = 0, chunk_src = 0, nchunk_src = 0, chunk_en = 0, nchunk_en = 0;
+  int64_t en_resident = 0;  // SMs x resident energy-kernel CTAs per SM (whole-wave chunk rule)
   // peer-store exchange of the products (bipb_p2p.cuh; BIPB_DIST_P2P / BIPB_EXCHANGE=p2p)
   bool p2p = false;
   double* p2p_box = nullptr;                // own mailbox [2][stride] (cudaMalloc: IPC-exportable)
@@ -274,6 +281,24 @@ static int64_t choose_chunk(int64_t ntgt_global, int64_t nsrc, int tgt_per_cta) 
   nchunk = std::min<int64_t>(nchunk, std::max<int64_t>(1, cdiv(nsrc, TILE)));
   int64_t chunk = cdiv(cdiv(nsrc, nchunk), TILE) * TILE;
   return std::max<int64_t>(chunk, TILE);
+}
+
+// Energy launch (few charge tiles x many element chunks): the chunk count is
+// rounded so that tiles x chunks fills whole waves of `resident` CTAs (r01 ncu: 2,340 CTAs over
+// 888 resident slots = 2.64 waves, FP64 pipe 77%).  Chunks stay >= one smem tile; below one wave
+// the rule is choose_chunk's.  `resident` is a device property (SMs x occupancy), equal on every
+// rank, so the sum order stays independent of the rank count.  BIPB_EN_WAVES=0 disables it (A/B).
+static int64_t choose_chunk_waves(int64_t ntgt_global, int64_t nsrc, int tgt_per_cta, int64_t resident) {
+  static const bool on = !(getenv("BIPB_EN_WAVES") && !strcmp(getenv("BIPB_EN_WAVES"), "0"));
+  if (!on || resident <= 0) return choose_chunk(ntgt_global, nsrc, tgt_per_cta);
+  const int64_t tiles = std::max<int64_t>(1, cdiv(ntgt_global, tgt_per_cta));
+  const int64_t cap = std::max<int64_t>(1, cdiv(nsrc, TILE));
+  int64_t want = std::min<int64_t>(std::max<int64_t>(32, cdiv(WANT_CTAS, tiles)), cap);
+  if (tiles * want >= resident) {
+    const int64_t waves = cdiv(tiles * want, resident);
+    want = std::min<int64_t>(cap, std::max<int64_t>(1, waves * resident / tiles));
+  }
+  return std::max<int64_t>(1, cdiv(nsrc, want));
 }
 
 static bool is_device_ptr(const void* p) {
@@ -893,7 +918,7 @@ static bipb_status load_charges(bipb_ctx* c, int64_t nc, const std::vector<doubl
   }
   c->chunk_src = choose_chunk(c->n, ncm, SRC_TPB * SRC_T);
   c->nchunk_src = cdiv(ncm, c->chunk_src);
-  c->chunk_en = choose_chunk(ncm, c->n, EN_TPB * EN_T);
+  c->chunk_en = choose_chunk_waves(ncm, c->n, EN_TPB * EN_T, c->en_resident);
   c->nchunk_en = cdiv(c->n, c->chunk_en);
   if (nc > 0) {  // a charge within 1e-6 A of a centroid (compared in scaled coordinates)
     CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
@@ -1108,6 +1133,23 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   if (const char* e = getenv("BIPB_COMM_TIMEOUT_S")) c->comm_timeout_ns = (unsigned long long)(atof(e) * 1e9);
   c->screened = kappa > 0.0;
   c->s = c->screened ? kappa : 1.0;
+  {  // resident energy-kernel CTAs on this device (whole-wave chunk rule, choose_chunk_waves)
+    const size_t en_smem = sizeof(double) * STAGES * TILE * 8 + 8 * STAGES;
+    int occ = 0, sms = 0, dev = 0;
+    cudaError_t oe = cudaGetDevice(&dev);
+    if (oe == cudaSuccess) oe = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (oe == cudaSuccess)
+      oe = c->screened
+               ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<ENERGY, EN_TPB, EN_T, true, EN_MINB>,
+                                                               EN_TPB, en_smem)
+               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<ENERGY, EN_TPB, EN_T, false, EN_MINB>,
+                                                               EN_TPB, en_smem);
+    if (oe != cudaSuccess) {
+      cudaGetLastError();
+      occ = 0;  // unknown: the plain chunk rule
+    }
+    c->en_resident = (int64_t)sms * occ;
+  }
   c->rank = dist ? dist->rank : 0;
   c->world = dist ? dist->world : 1;
   c->sharded = dist != nullptr;

@@ -44,6 +44,9 @@ for w in $WHAT; do
       done ;;
     shards)
       timeout 900 python tools/shard_scaling.py C4 > $O/shard_scaling_C4.jsonl 2>&1; cat $O/shard_scaling_C4.jsonl ;;
+    energy)
+      python tools/tune_energy.py run C4 20 > $O/tune_energy_C4.jsonl 2> $O/tune_energy_C4.err; cat $O/tune_energy_C4.jsonl
+      python tools/tune_energy.py run C3 50 > $O/tune_energy_C3.jsonl 2> $O/tune_energy_C3.err; cat $O/tune_energy_C3.jsonl ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
         python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --precond-steps 0 > /dev/null 2>&1 ;;
