@@ -39,8 +39,10 @@ namespace bipb {
 // record prefetch of the 32-step rotation, per number of operands: 1 = load the next step's
 // record while this one computes (register copy per step), 2 = ping-pong buffers (no copies, two
 // records live), 0 = load at the top of each step (no copies, load latency exposed)
+// (r02 session 4, profiles/r02/session4/tune_batch_C4.jsonl: ping-pong for R > 1 -- R = 4 320.4 ->
+// 317.4 ms, R = 2 236.6 -> 235.1 per C4 product; R = 1 keeps 1: 191.1 vs 201.9 ms with 2, 198.1 with 0)
 #ifndef BIPB_SYM_PREFETCH_MRHS
-#define BIPB_SYM_PREFETCH_MRHS BIPB_SYM_PREFETCH
+#define BIPB_SYM_PREFETCH_MRHS 2
 #endif
 __host__ __device__ constexpr int sym_prefetch(int R) { return R == 1 ? BIPB_SYM_PREFETCH : BIPB_SYM_PREFETCH_MRHS; }
 

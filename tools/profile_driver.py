@@ -17,6 +17,7 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 2
 p = g.config(cfg)
 ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa)
 u = g.random_vector(2 * p.n, 1)
+y = u
 for _ in range(reps):
     y = bp.bipb_matvec(ctx, u)
 if "--all" in sys.argv:
