@@ -241,6 +241,19 @@ int32_t bipb_get_exchange(bipb_ctx* ctx);
 int32_t bipb_get_arnoldi(bipb_ctx* ctx);
 
 /*
+ * Device-side GMRES cycles (an execution mode of bipb_gmres_solve, Table 1 steps 9-16; opt-in with
+ * BIPB_GRAPHS=2 in the environment): the m Arnoldi steps of a cycle run as ONE CUDA-graph launch,
+ * each step in a conditional (IF) node that a one-thread kernel clears once the host loop would
+ * leave the cycle (breakdown, convergence, max_iters, NaN), and the host reads the per-step
+ * residual records once per cycle.  Results are bitwise those of the eager loop.  Used on
+ * single-GPU contexts after one eager product (a graph capture cannot allocate); if the graph
+ * cannot be built the context falls back to eager cycles for good.
+ * Returns the number of cycles this context has run as graphs (0 when the mode is off), -1 for a
+ * NULL context.
+ */
+int64_t bipb_get_graph_cycles(bipb_ctx* ctx);
+
+/*
  * GMRES preconditioning (NOT in the paper, which runs plain GMRES; default 0):
  *   0  plain GMRES(m) (the paper's method; parity with the oracle's iteration counts)
  *   1  right preconditioning by the diagonal of the jump terms of Eqs. (12)-(13),

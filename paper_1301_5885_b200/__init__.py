@@ -76,6 +76,7 @@ _SIGS = {
     "bipb_get_matvec_kernel": ([_P], _I32),
     "bipb_get_exchange": ([_P], _I32),
     "bipb_get_arnoldi": ([_P], _I32),
+    "bipb_get_graph_cycles": ([_P], _I64),
     "bipb_set_precond": ([_P, _I32], ctypes.c_int),
     "bipb_get_precond": ([_P], _I32),
     "bipb_set_sum_mode": ([_P, _I32], ctypes.c_int),
@@ -202,6 +203,11 @@ class Context:
     @property
     def sum_mode(self) -> int:
         return int(_lib.bipb_get_sum_mode(self.handle))
+
+    @property
+    def graph_cycles(self) -> int:
+        """GMRES cycles this context ran as one CUDA-graph launch (BIPB_GRAPHS=2; bipb.h)."""
+        return int(_lib.bipb_get_graph_cycles(self.handle))
 
     @property
     def arnoldi(self) -> int:
@@ -383,6 +389,11 @@ def bipb_get_sum_mode(ctx: Context) -> int:
 def bipb_get_arnoldi(ctx: Context) -> int:
     """0 multi-launch MGS, E > 0 fused cluster Arnoldi kernel (bipb.h)."""
     return int(_lib.bipb_get_arnoldi(ctx.handle))
+
+
+def bipb_get_graph_cycles(ctx: Context) -> int:
+    """GMRES cycles run as one CUDA-graph launch (BIPB_GRAPHS=2; bipb.h)."""
+    return int(_lib.bipb_get_graph_cycles(ctx.handle))
 
 
 def bipb_destroy(ctx: Context):

@@ -257,6 +257,20 @@ struct bipb_ctx {
     int m = 0, kind = -1, precond = -1, exact = -1;
     std::vector<cudaGraphExec_t> ex;
   } ag;
+  // BIPB_GRAPHS=2: one graph per Arnoldi cycle (m IF nodes, each one step + cycle_check_kernel),
+  // same validity key as `ag`; cyc = device [8 + 2m] (parameters, per-step records), cyc_host its
+  // pinned copy
+  struct {
+    const double* V = nullptr;
+    int m = 0, kind = -1, precond = -1, exact = -1;
+    cudaGraphExec_t ex = nullptr;
+  } cg;
+  double* cyc = nullptr;
+  double* cyc_host = nullptr;
+  int cyc_cap = 0;
+  int64_t graph_cycles = 0;  // cycles run as one graph launch (bipb_get_graph_cycles)
+  bool cycle_off = false;  // the cycle graph could not be built here: eager cycles from then on
+  std::string cycle_err;
 };
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -411,6 +425,9 @@ static void drop_graphs(bipb_ctx* c) {
     if (e) cudaGraphExecDestroy(e);
   c->ag.ex.clear();
   c->ag.V = nullptr;  // forces a rebuild on the next solve
+  if (c->cg.ex) cudaGraphExecDestroy(c->cg.ex);
+  c->cg.ex = nullptr;
+  c->cg.V = nullptr;
 }
 
 // chunk-partial scratch of the row kernel / source / energy, grown on demand.  A reallocation
@@ -867,6 +884,9 @@ void bipb_destroy(bipb_ctx* c) {
     for (auto e : p.ev) cudaEventDestroy(e);
   for (auto e : c->ag.ex)
     if (e) cudaGraphExecDestroy(e);
+  if (c->cg.ex) cudaGraphExecDestroy(c->cg.ex);
+  if (c->cyc) dfree(c, c->cyc);
+  if (c->cyc_host) cudaFreeHost(c->cyc_host);
   if (c->comm && nccl().ok) {
     if (c->failed && nccl().CommAbort)
       nccl().CommAbort(c->comm);
@@ -1397,7 +1417,7 @@ static bipb_status ensure_krylov(bipb_ctx* c, int m) {
 // modified Gram-Schmidt; Givens update; the 16-byte residual record copied to pinned host
 // memory; w /= h_{k+1,k} (harmless garbage on a happy breakdown: V[k+1] is then unused).
 // Enqueue only (no synchronisation) so it can be captured as a CUDA graph.
-static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
+static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m, bool cycle = false) {
   const int64_t m2 = 2 * c->n;
   double* S = c->scal;
   double* vk = c->V + (int64_t)k * m2;
@@ -1417,7 +1437,7 @@ static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
     }
     c->launches_all++;
     CK(cudaGetLastError());
-    if (!c->host_info_dev)
+    if (!c->host_info_dev && !cycle)
       CK(cudaMemcpyAsync(c->host_info, S + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     return BIPB_OK;
   }
@@ -1434,7 +1454,7 @@ static bipb_status enqueue_arnoldi_step(bipb_ctx* c, int k, int m) {
   CK(cudaGetLastError());
   givens_kernel<<<1, 1, 0, c->stream>>>(c->H, c->cs, c->sn, c->g, S + 2, S + 3, k, m, S + 0, S + 6);
   c->launches_all++;
-  CK(cudaMemcpyAsync(c->host_info, S + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (!cycle) CK(cudaMemcpyAsync(c->host_info, S + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   LAUNCH1D(scale_div_kernel, m2, w, w, S + 3, m2);
   return BIPB_OK;
 }
@@ -1483,6 +1503,151 @@ static bipb_status run_arnoldi_step(bipb_ctx* c, int k, int m, double* h2) {
   CKS(ctx_sync(c));
   h2[0] = c->host_info[0];
   h2[1] = c->host_info[1];
+  return BIPB_OK;
+}
+
+// ---- device-side Arnoldi cycle (BIPB_GRAPHS=2): the m steps of a GMRES(m) cycle as ONE graph
+// launch. Step k sits in an IF node on a condition that cycle_check_kernel clears when the host
+// loop would leave the cycle after that step (breakdown, convergence, iteration cap, NaN), so the
+// later steps do not run; the host reads the per-step records once per cycle instead of once per
+// step. Single-GPU contexts only (the multi-rank exchange's collectives stay out of conditional
+// bodies), after an eager product has prepared the product's buffers (capture cannot allocate).
+static bool cycle_usable(const bipb_ctx* c) {
+  static const bool on = getenv("BIPB_GRAPHS") && !strcmp(getenv("BIPB_GRAPHS"), "2");
+  return on && !c->cycle_off && c->world == 1 && !c->timing && c->warm_kind == warm_key(c);
+}
+
+// Sink nodes of a graph (no dependents): the dependencies of the node appended after them.
+static cudaError_t graph_sinks(cudaGraph_t g, std::vector<cudaGraphNode_t>& out) {
+  out.clear();
+  size_t n = 0;
+  cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+  if (e != cudaSuccess || n == 0) return e;
+  std::vector<cudaGraphNode_t> nodes(n);
+  e = cudaGraphGetNodes(g, nodes.data(), &n);
+  for (size_t i = 0; i < n && e == cudaSuccess; ++i) {
+    size_t d = 0;
+    e = cudaGraphNodeGetDependentNodes(nodes[i], nullptr, &d);
+    if (e == cudaSuccess && d == 0) out.push_back(nodes[i]);
+  }
+  return e;
+}
+
+// The cycle graph: IF(c_0){ step 0; check 0; IF(c_1){ step 1; check 1; IF(c_2){ ... } } } -- the
+// IF nodes are nested because a conditional handle belongs to ONE node: c_0 (top level) defaults
+// to 1 at every launch, c_{k+1} is created in step k's body and always written by check k (1 to
+// go on, 0 to leave the cycle), so no value from an earlier launch is ever read.
+static bipb_status build_cycle_graph(bipb_ctx* c, int m) {
+  const int exact = exact_active(c) ? 1 : 0;
+  if (c->cg.ex && c->cg.V == c->V && c->cg.m == m && c->cg.kind == c->mv_kind && c->cg.precond == c->precond &&
+      c->cg.exact == exact)
+    return BIPB_OK;
+  if (c->cg.ex) cudaGraphExecDestroy(c->cg.ex);
+  c->cg.ex = nullptr;
+  c->cg.V = nullptr;
+  cudaGraph_t g = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  bipb_status st = BIPB_OK;
+  std::string what = "conditional handle 0";
+  cudaGraphConditionalHandle cond = 0;
+  cudaError_t ce = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+  cudaGraph_t parent = g;
+  std::vector<cudaGraphNode_t> deps;
+  for (int k = 0; k < m && ce == cudaSuccess && st == BIPB_OK; ++k) {
+    what = "conditional node " + std::to_string(k);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t node = nullptr;
+    ce = cudaGraphAddNode(&node, parent, deps.empty() ? nullptr : deps.data(), deps.size(), &np);
+    if (ce != cudaSuccess) break;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle next = 0;
+    if (k + 1 < m) {
+      what = "conditional handle " + std::to_string(k + 1);
+      ce = cudaGraphConditionalHandleCreate(&next, body, 0, 0);
+      if (ce != cudaSuccess) break;
+    }
+    what = "begin capture " + std::to_string(k);
+    ce = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) break;
+    st = enqueue_arnoldi_step(c, k, m, true);
+    if (st == BIPB_OK) {
+      cycle_check_kernel<<<1, 1, 0, c->stream>>>(c->scal, c->cyc, k, next, k + 1 < m ? 1 : 0);
+      ce = cudaGetLastError();
+    }
+    if (ce != cudaSuccess) what = "step capture " + std::to_string(k);
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(c->stream, &captured);
+    if (ce == cudaSuccess && ee != cudaSuccess) {
+      ce = ee;
+      what = "end capture " + std::to_string(k);
+    }
+    if (ce == cudaSuccess) {
+      what = "sinks " + std::to_string(k);
+      ce = graph_sinks(body, deps);
+    }
+    parent = body;
+    cond = next;
+  }
+  cudaGraphExec_t ex = nullptr;
+  if (ce == cudaSuccess && st == BIPB_OK) {
+    what = "instantiate";
+    ce = cudaGraphInstantiate(&ex, g, 0);
+  }
+  cudaGraphDestroy(g);
+  if (st != BIPB_OK) return st;
+  if (ce != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BIPB_ERR_CUDA, "cycle graph (" + what + "): " + cudaGetErrorString(ce));
+  }
+  c->cg.ex = ex;
+  c->cg.V = c->V;
+  c->cg.m = m;
+  c->cg.kind = c->mv_kind;
+  c->cg.precond = c->precond;
+  c->cg.exact = exact;
+  return BIPB_OK;
+}
+
+// One cycle on the device: parameters in, the graph, the per-step records (rel, h_{k+1,k}) out
+// into c->cyc_host[8 ..]; the caller replays the host loop's bookkeeping on them.
+static bipb_status run_cycle(bipb_ctx* c, int m, double beta_b, double tol, int64_t its, int max_iters, bool exact,
+                             bool* ran) {
+  NvtxRange nvtx_("arnoldi_cycle");
+  *ran = false;
+  if (c->cyc_cap < m) {
+    if (c->cyc) dfree(c, c->cyc);
+    if (c->cyc_host) cudaFreeHost(c->cyc_host);
+    c->cyc = nullptr;
+    c->cyc_host = nullptr;
+    c->cyc_cap = 0;
+    CK(dmalloc(c, &c->cyc, (size_t)(8 + 2 * m) * sizeof(double)));
+    CK(cudaMallocHost(&c->cyc_host, (size_t)(8 + 2 * m) * sizeof(double)));
+    c->cyc_cap = m;
+    if (c->cg.ex) cudaGraphExecDestroy(c->cg.ex);  // it holds the old c->cyc
+    c->cg.ex = nullptr;
+  }
+  if (build_cycle_graph(c, m) != BIPB_OK) {  // e.g. a node type the driver rejects in a conditional body
+    c->cycle_off = true;
+    c->cycle_err = g_err;
+    if (getenv("BIPB_CYCLE_VERBOSE")) fprintf(stderr, "[bipb] cycle graphs off: %s\n", g_err.c_str());
+    return BIPB_OK;  // the caller runs this cycle eagerly
+  }
+  double* h = c->cyc_host;
+  h[0] = beta_b;
+  h[1] = tol;
+  h[2] = (double)its;
+  h[3] = (double)max_iters;
+  h[4] = exact ? 1.0 : 0.0;
+  CK(cudaMemcpyAsync(c->cyc, h, 8 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaGraphLaunch(c->cg.ex, c->stream));
+  CK(cudaMemcpyAsync(h + 8, c->cyc + 8, 2 * m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CKS(ctx_sync(c));
+  *ran = true;
+  c->graph_cycles++;
   return BIPB_OK;
 }
 
@@ -1747,8 +1912,15 @@ rerun:
       init_g_kernel<<<1, 32, 0, c->stream>>>(c->g, S + 1, m);
       c->launches_all++;
       int kdone = 0;
+      bool cycle = false;
+      if (cycle_usable(c)) CKS(run_cycle(c, m, beta_b, tol, its, max_iters, exact, &cycle));
       for (int k = 0; k < m; ++k) {
-        CKS(run_arnoldi_step(c, k, m, h2));
+        if (cycle) {
+          h2[0] = c->cyc_host[8 + 2 * k];
+          h2[1] = c->cyc_host[9 + 2 * k];
+        } else {
+          CKS(run_arnoldi_step(c, k, m, h2));
+        }
         ++matvecs;
         ++its;
         rel = h2[0];
@@ -1956,6 +2128,8 @@ bipb_status bipb_set_matvec_kernel(bipb_ctx* c, int32_t kind) {
 int32_t bipb_get_matvec_kernel(bipb_ctx* c) { return c ? c->mv_kind : -1; }
 
 int32_t bipb_get_arnoldi(bipb_ctx* c) { return c ? c->arn_E : -1; }
+
+int64_t bipb_get_graph_cycles(bipb_ctx* c) { return c ? c->graph_cycles : -1; }
 
 bipb_status bipb_set_precond(bipb_ctx* c, int32_t kind) {
   if (!c) return fail(BIPB_ERR_ARG, "ctx is NULL");

@@ -220,6 +220,22 @@ __device__ __forceinline__ void givens_step(double* H, double* cs, double* sn, d
   info[0] = fabs(g[k + 1]) / beta_b;
   info[1] = h;
 }
+// Device-side Arnoldi cycle (BIPB_GRAPHS=2, bipb.cu run_cycle): after step k of a cycle graph,
+// record the step's (|g_{k+1}|/beta_b, h_{k+1,k}) = S[6], S[7] in cyc[8 + 2k ..] and, when the host
+// loop of bipb_gmres_solve would leave the cycle here, set the next step's IF condition to 0 (else
+// to 1) so the remaining steps do not run.  The tests are the host loop's, on the same doubles:
+// happy breakdown h_{k+1,k} <= 1e-14 beta_b, |g|/beta_b <= tol, its >= max_iters, NaN (exact sums).
+// cyc[0..4] = beta_b, tol, iterations before the cycle, max_iters, exact-sums flag.
+__global__ void cycle_check_kernel(const double* __restrict__ S, double* __restrict__ cyc, int k,
+                                   cudaGraphConditionalHandle next, int has_next) {
+  const double rel = S[6], hk1 = S[7];
+  cyc[8 + 2 * k] = rel;
+  cyc[9 + 2 * k] = hk1;
+  const bool stop = (hk1 <= 1e-14 * cyc[0]) || (rel <= cyc[1]) || (cyc[2] + (k + 1) >= cyc[3]) ||
+                    (cyc[4] != 0.0 && !(rel == rel));
+  if (has_next) cudaGraphSetConditional(next, stop ? 0u : 1u);
+}
+
 __global__ void givens_kernel(double* H, double* cs, double* sn, double* g, const double* hk1sq, double* hk1,
                               int k, int m, const double* beta_b_ptr, double* info) {
   givens_step(H, cs, sn, g, *hk1sq, hk1, k, m, *beta_b_ptr, info);

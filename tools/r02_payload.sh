@@ -47,6 +47,13 @@ for w in $WHAT; do
     energy)
       python tools/tune_energy.py run C4 20 > $O/tune_energy_C4.jsonl 2> $O/tune_energy_C4.err; cat $O/tune_energy_C4.jsonl
       python tools/tune_energy.py run C3 50 > $O/tune_energy_C3.jsonl 2> $O/tune_energy_C3.err; cat $O/tune_energy_C3.jsonl ;;
+    cycle)
+      timeout 900 python -m pytest tests/test_gpu_cycle.py -m gpu -q -p no:cacheprovider -rfEs > $O/pytest_cycle.txt 2>&1
+      tail -3 $O/pytest_cycle.txt
+      for gm in 0 1 2; do
+        BIPB_GRAPHS=$gm timeout 600 python tools/gmres_overhead.py C1 C2 C3 > $O/gmres_overhead_g$gm.txt 2>&1
+        cat $O/gmres_overhead_g$gm.txt
+      done ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
         python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --precond-steps 0 > /dev/null 2>&1 ;;
