@@ -29,11 +29,13 @@ VARIANTS = []
 # speed probe only, exact at C4 which has no padded rows), and the baseline twice for the noise.
 # The multi-RHS kernels (R = 2, 4) spend ~16 register moves per pair on the prefetched record copy
 # (40 IMAD.MOV per R = 4 step): PREFETCH = 0 / 2 are timed for them too (`runbatch`).
-for t, minb, un, rs, pf, nc in ((5, 1, 1, 0, 1, 0), (5, 1, 1, 0, 2, 0), (5, 1, 1, 0, 1, 1), (5, 1, 1, 1, 1, 0),
-                                (5, 1, 1, 0, 2, 1), (5, 1, 1, 0, 0, 0), (5, 1, 1, 0, 1, 0)):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": minb, "exp_bits": 11, "pf": pf, "un": 1,
+# (session-3 set, measured in r02 session 4: profiles/r02/session4/tune_sym_C4.jsonl -- all slower
+# than or equal to the default.)  Session 4: CTA size at 8 warps per SM -- one 256-thread CTA
+# (B = 1280, per-stage reverse combine to fit the shared memory) or four 64-thread CTAs (B = 256, T = 4).
+for tpb, t, minb, rs in ((128, 5, 1, 0), (256, 5, 1, 1), (64, 4, 4, 0), (128, 5, 1, 0)):
+    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
                      "tile": 128, "stages": 3,
-                     "defs": {"BIPB_SYM_STUNROLL": un, "BIPB_SYM_RS_STAGE": rs, "BIPB_EXP_NOCLAMP": nc}})
+                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": rs}})
 
 
 def name(v):
