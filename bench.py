@@ -69,6 +69,25 @@ def parse():
     return ap.parse_args()
 
 
+def golden_check(prob, energy, iterations):
+    """The timed solve against the stored full oracle solve of the same input (tests/golden/oracle_<cfg>.json,
+    written by tests/make_oracle_golden.py from oracle/ alone; a JSON read, no oracle code runs here):
+    north_star's parity bar -- E_sol within 1e-8 relative, iterations within +-1 -- checked on every
+    bench line, also on every rank count (a broken multi-GPU exchange shows up here)."""
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_{prob.name.split('_')[0]}.json")
+    try:
+        gold = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    ref = gold.get("solves", {}).get(str(RESTART_M))
+    if gold.get("sha256") != prob.sha256() or gold.get("tol") != TOL or not ref:
+        return None
+    rel = abs(energy / ref["energy"] - 1.0)
+    return {"file": os.path.relpath(path, ROOT), "energy_kcal_mol": ref["energy"], "iterations": ref["iterations"],
+            "energy_rel_diff": rel, "iterations_diff": int(iterations) - int(ref["iterations"]),
+            "pass": bool(rel <= 1e-8 and abs(int(iterations) - int(ref["iterations"])) <= 1)}
+
+
 def bench_config(prob, world):
     return {"workload": prob.name, "n_elements": prob.n, "n_charges": prob.nc, "restart_m": RESTART_M, "tol": TOL,
             "eps1": prob.eps1, "eps2": prob.eps2, "kappa": prob.kappa,
@@ -352,6 +371,9 @@ def run_native(args):
             "energy_kcal_mol": e_box[-1], "gpu_launches": int(all_launches),
             "kernel_ms": {"matvec": mv_ms, "source": src_ms, "energy": en_ms, "steps_sum": sum(per_step_ms)},
             "roofline": roofline, "clocks": clocks}
+    gold = golden_check(prob, e_box[-1], reps[-1]["iterations"])
+    if gold:
+        line["oracle_golden"] = gold
 
     # ---- paper-like tolerance ("one tol = 1e-4 run per config"; Table 4 N_it 9-11)
     if args.paper_tol_steps > 0:

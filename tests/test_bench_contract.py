@@ -51,6 +51,8 @@ def test_native_arm_json():
     assert d["cpu_baseline"]["kind"] == "oracle"
     pc = d["precond"]  # the opt-in preconditioned solve, beside the headline
     assert pc["energy_rel_diff_vs_plain"] <= 1e-8 and max(pc["iterations"]) < min(d["iterations"])
+    og = d["oracle_golden"]  # the timed solve against tests/golden/oracle_C2.json
+    assert og["pass"] and og["energy_rel_diff"] <= 1e-8 and abs(og["iterations_diff"]) <= 1
 
 
 @pytest.mark.gpu
@@ -69,3 +71,4 @@ def test_native_arm_two_ranks_one_gpu():
     d = json.loads(lines[0])
     assert REQUIRED <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "strong" and "cpu_baseline" not in d
     assert d["exchange"] == "p2p"  # default: peer stores (both ranks map each other's mailbox)
+    assert d["oracle_golden"]["pass"]  # the 2-rank solve against the stored oracle solve
