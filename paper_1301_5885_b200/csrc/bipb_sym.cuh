@@ -181,8 +181,14 @@ __device__ __forceinline__ void pair_sym(const SymSrc<R>& ti, const SymSrc<R>& s
   }
 }
 
+// BIPB_SYM_MAXNREG (tuning probe only): a per-kernel register cap instead of the occupancy bound
+#ifdef BIPB_SYM_MAXNREG
+#define BIPB_SYM_BOUNDS(TPB, MINB) __maxnreg__(BIPB_SYM_MAXNREG)
+#else
+#define BIPB_SYM_BOUNDS(TPB, MINB) __launch_bounds__(TPB, MINB)
+#endif
 template <int TPB, int T, bool SCREENED, int MINB, int R, bool EXACT = false>
-__global__ void __launch_bounds__(TPB, MINB) sym_kernel(const SymArgs a) {
+__global__ void BIPB_SYM_BOUNDS(TPB, MINB) sym_kernel(const SymArgs a) {
   static_assert(!EXACT || R == 1, "exact sums: single operand only");
   constexpr int NW = TPB / 32;
   constexpr int B = TPB * T;

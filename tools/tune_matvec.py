@@ -32,16 +32,19 @@ VARIANTS = []
 # (session-3 set, measured in r02 session 4: profiles/r02/session4/tune_sym_C4.jsonl -- all slower
 # than or equal to the default.)  Session 4: CTA size at 8 warps per SM -- one 256-thread CTA
 # (B = 1280, per-stage reverse combine to fit the shared memory) or four 64-thread CTAs (B = 256, T = 4).
-for tpb, t, minb, rs in ((128, 5, 1, 0), (256, 5, 1, 1), (64, 4, 4, 0), (128, 5, 1, 0)):
-    VARIANTS.append({"kind": "sym", "tpb": tpb, "t": t, "minb": minb, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3,
-                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": rs}})
+# (measured: profiles/r02/session4/tune_sym_cta_C4.jsonl, both slower.)  Then a register-cap sweep
+# (__maxnreg__, BIPB_SYM_MAXNREG: the same code, ptxas schedules the five pair chains under a tighter budget).
+for mr in (0, 224, 208, 192, 0):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
+                     "tile": 128, "stages": 3, "maxrreg": mr,
+                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0}})
 
 
 def name(v):
     extra = "".join(f"_{k.replace('BIPB_', '').lower()}{val}" for k, val in sorted(v.get("defs", {}).items()))
     return (f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}"
-            f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}{extra}")
+            f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}{extra}"
+            + (f"_mr{v['maxrreg']}" if v.get("maxrreg") else ""))
 
 
 def build():
@@ -58,6 +61,8 @@ def build():
                      f"-DBIPB_SYM_UNROLL={v.get('un', 1)}", f"-DBIPB_TILE={v.get('tile', 128)}",
                      f"-DBIPB_STAGES={v.get('stages', 3)}"]
             extra += [f"-D{k}={val}" for k, val in v.get("defs", {}).items()]
+            if v.get("maxrreg"):
+                extra += [f"-DBIPB_SYM_MAXNREG={v['maxrreg']}"]
         else:
             extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}"]
