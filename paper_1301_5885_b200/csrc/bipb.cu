@@ -69,12 +69,31 @@ struct SymCfg<4> {
 // R = 1 on mid-size problems (fewer than SYM_SMALL_TASKS block pairs at T = 5): smaller blocks,
 // 3 CTAs per SM -- more, shorter (I, J) tasks balance better over 148 SMs (measured: C2 product
 // 0.966 -> 0.863 ms; C3/C4 are faster at T = 5; profiles/r01/tune_shape_C*.jsonl)
+#ifndef BIPB_SYMMID_T
+#define BIPB_SYMMID_T 3
+#endif
+#ifndef BIPB_SYMMID_MINB
+#define BIPB_SYMMID_MINB 3
+#endif
 struct SymCfgMid {
-  static constexpr int TPB = 128, T = 3, MINB = 3;
+  static constexpr int TPB = 128, T = BIPB_SYMMID_T, MINB = BIPB_SYMMID_MINB;
 };
+// R = 1 on small problems (fewer than SYM_MID_TASKS block pairs at B = 384, e.g. C1): one target per
+// thread, B = 128, 4 CTAs per SM -- enough (I, J) tasks to fill the machine (C1: 840 tasks; product
+// 89 us vs 107 us for the row kernel and 153 us at B = 384, profiles/r02/session4/tune_small_C*.jsonl)
+struct SymCfgSmall {
+  static constexpr int TPB = 128, T = 1, MINB = 4;
+};
+constexpr int64_t SYM_MID_TASKS = 1024;
+constexpr int64_t SYM_MIN_TASKS = 296;  // default kernel: symmetric from this many B = 128 tasks on
+static int64_t sym_tasks(int64_t n, int64_t B) {
+  const int64_t nb = (n + B - 1) / B;
+  return nb * (((nb & 1) ? (nb - 1) / 2 : nb / 2) + 1);
+}
 constexpr int64_t SYM_SMALL_TASKS = 2048;
 static_assert((SymCfg<1>::TPB * SymCfg<1>::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 static_assert((SymCfgMid::TPB * SymCfgMid::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
+static_assert((SymCfgSmall::TPB * SymCfgSmall::T) % TILE == 0, "symmetric block must be a multiple of the smem tile");
 constexpr int SRC_TPB = 128, SRC_T = 2, SRC_MINB = 4;
 #ifndef BIPB_EN_T
 #define BIPB_EN_T 4  // r02 A/B (profiles/r02/session4/tune_energy_C*.jsonl): C4 3.69 -> 3.40 ms with the wave rule
@@ -566,9 +585,9 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   constexpr int F = SymLayout<R>::F;
   const int64_t n = c->n;
   int64_t B = SymCfg<R>::TPB * SymCfg<R>::T;
-  if (R == 1) {
-    const int64_t nb5 = cdiv(n, B), h5 = (nb5 & 1) ? (nb5 - 1) / 2 : nb5 / 2;
-    if (nb5 * (h5 + 1) < SYM_SMALL_TASKS) B = SymCfgMid::TPB * SymCfgMid::T;
+  if (R == 1 && sym_tasks(n, B) < SYM_SMALL_TASKS) {  // fewer, larger tasks than the machine wants
+    B = SymCfgMid::TPB * SymCfgMid::T;
+    if (sym_tasks(n, B) < SYM_MID_TASKS) B = SymCfgSmall::TPB * SymCfgSmall::T;
   }
   p.B = B;
   p.nb = cdiv(n, B);
@@ -676,14 +695,22 @@ static bipb_status matvec_sym_R(bipb_ctx* c, const double* U, double* Y, bool al
     CKS(timed_begin(c, 0, &stop));
     bool mid = false;
     if constexpr (R == 1) {
-      if (p->B == SymCfgMid::TPB * SymCfgMid::T) {
-        using M = SymCfgMid;
+      // the smaller R = 1 block shapes (mid-size and small problems)
+      auto launch_shape = [&](auto shape) -> bipb_status {
+        using M = decltype(shape);
         auto k = c->screened ? (exact ? sym_kernel<M::TPB, M::T, true, M::MINB, R, R == 1>
                                       : sym_kernel<M::TPB, M::T, true, M::MINB, R>)
                              : (exact ? sym_kernel<M::TPB, M::T, false, M::MINB, R, R == 1>
                                       : sym_kernel<M::TPB, M::T, false, M::MINB, R>);
         CKS(set_smem(k, smem));
         k<<<(unsigned)grid, M::TPB, smem, c->stream>>>(a);
+        return BIPB_OK;
+      };
+      if (p->B == SymCfgMid::TPB * SymCfgMid::T) {
+        CKS(launch_shape(SymCfgMid{}));
+        mid = true;
+      } else if (p->B == SymCfgSmall::TPB * SymCfgSmall::T) {
+        CKS(launch_shape(SymCfgSmall{}));
         mid = true;
       }
     }
@@ -1241,10 +1268,12 @@ static bipb_status setup_impl(bipb_ctx* c, int64_t n, const double* centroids, c
   // kernel (small problems); BIPB_MATVEC=row|sym overrides.  Symmetric buffers are allocated on
   // first use (sym_plan).
   {
-    const int64_t nb1 = cdiv(n, (int64_t)SymCfg<1>::TPB * SymCfg<1>::T);
-    const int64_t h1 = (nb1 & 1) ? (nb1 - 1) / 2 : nb1 / 2;
-    c->mv_kind = (nb1 * (h1 + 1) >= 2 * 148) ? 1 : 0;  // measured: C1 (40 tiles) row 0.13 ms vs sym 0.34;
-                                                       // C2 (544 tiles) sym 0.98 ms vs row 1.45
+    // r02 session 4: with the small block shape (B = 128) the symmetric kernel wins from C1 on
+    // (C1 product 89 vs 107 us, C2 0.88 vs 1.36 ms); below SYM_MIN_TASKS small-shape tasks the row
+    // kernel (profiles/r02/session4/small_sizes.jsonl)
+    int64_t min_tasks = SYM_MIN_TASKS;
+    if (const char* e = getenv("BIPB_SYM_MIN_TASKS")) min_tasks = atoll(e);  // tuning
+    c->mv_kind = (sym_tasks(n, SymCfgSmall::TPB * SymCfgSmall::T) >= min_tasks) ? 1 : 0;
     const char* env = getenv("BIPB_MATVEC");
     if (env && (!strcmp(env, "row") || !strcmp(env, "0"))) c->mv_kind = 0;
     if (env && (!strcmp(env, "sym") || !strcmp(env, "1"))) c->mv_kind = 1;

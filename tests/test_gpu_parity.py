@@ -373,9 +373,9 @@ def test_symmetric_shards_sum_to_single_gpu(bp, world):
     assert _rel(acc + du, y1) <= 1e-14
 
 
-@pytest.mark.parametrize("n_keep", [1, 2, 383, 384, 385, 767, 768, 769, 1151, 1536, 2047, 2560, 5119])
+@pytest.mark.parametrize("n_keep", [1, 2, 127, 128, 129, 255, 256, 257, 383, 384, 385, 1151, 1536, 2047, 2560, 5119])
 def test_symmetric_block_edges(bp, n_keep):
-    """Ragged block counts around the mid-size block B = 384 (the shape every N below ~40k gets):
+    """Ragged block counts around the small block B = 128 (the shape every N below ~17k gets, r02):
     nb = 1, 2 with an exactly full / one-row last block, odd and even nb, partial last block."""
     p = _ragged(4, 4.0, n_keep, 3, np.zeros((0, 4))) if n_keep > 1 else g.Problem(
         "n1", np.array([[1.0, 0, 0]]), np.array([[1.0, 0, 0]]), np.array([0.3]), np.zeros((0, 4)))
@@ -543,6 +543,33 @@ def test_fused_arnoldi_size_rule(bp):
         p = _ragged(6, 4.0, keep, 5, q)
         ctx = _ctx(bp, p)
         assert ctx.arnoldi == want
+        ctx.close()
+
+
+@pytest.mark.parametrize("n_keep", [17279, 17280, 17281])
+def test_symmetric_block_edges_b384(bp, n_keep):
+    """Block edges of the mid-size shape B = 384 (>= 1,024 tasks at B = 384, < 2,048 at B = 640):
+    N = 45*384 - 1, 45*384, 45*384 + 1 (nb = 45 with a one-row-short / full last block, nb = 46 with
+    a one-row last block).  The whole product against the oracle, per block and element-wise."""
+    p = _ragged(6, 20.0, n_keep, 13, np.zeros((0, 4)))
+    ctx = _ctx(bp, p)
+    assert ctx.matvec_kernel == 1
+    u = g.random_vector(2 * p.n, 8)
+    y = bp.bipb_matvec(ctx, u)
+    ctx.close()
+    ref = oracle.matvec(p, u)
+    for h in (slice(0, p.n), slice(p.n, 2 * p.n)):
+        assert _rel(y[h], ref[h]) <= 1e-11
+        assert np.max(np.abs(y[h] - ref[h])) <= 1e-11 * np.max(np.abs(ref[h]))
+
+
+def test_default_kernel_rule(bp):
+    """The default product (r02): the row kernel below 296 small-shape (B = 128) tasks, the symmetric
+    kernel from there on (N = 2,560: 220 tasks -> row; N = 3,840: 480 -> symmetric; C1 5,120)."""
+    for n_keep, want in ((2560, 0), (3840, 1), (5120, 1)):
+        p = _ragged(4, 4.0, n_keep, 5, np.zeros((0, 4))) if n_keep < 5120 else g.config("C1")
+        ctx = _ctx(bp, p)
+        assert ctx.matvec_kernel == want, n_keep
         ctx.close()
 
 

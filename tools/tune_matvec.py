@@ -34,11 +34,15 @@ VARIANTS = []
 # (B = 1280, per-stage reverse combine to fit the shared memory) or four 64-thread CTAs (B = 256, T = 4).
 # (measured: profiles/r02/session4/tune_sym_cta_C4.jsonl, both slower.)  Then a register-cap sweep
 # (__maxnreg__, BIPB_SYM_MAXNREG: the same code, ptxas schedules the five pair chains under a tighter budget).
-# (measured: tune_sym_maxnreg_C4.jsonl, all slower.)  Then T = 6 (252 registers, no spills, B = 768).
-for t, rs in ((5, 0), (6, 0), (6, 1), (5, 0)):
-    VARIANTS.append({"kind": "sym", "tpb": 128, "t": t, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
+# (measured: tune_sym_maxnreg_C4.jsonl, all slower; T = 6: tune_sym_t6_C4.jsonl, slower.)
+# Small problems (C1, C2): the symmetric kernel with small blocks (the mid-size shape, chosen below
+# 2,048 block pairs at B = 640, at T = 1 / 2 / 3, i.e. B = 128 / 256 / 384) against the row kernel.
+VARIANTS.append({"kind": "row", "tpb": 128, "t": 3, "minb": 3, "exp_bits": 11})
+for mt, mb in ((1, 4), (2, 4), (3, 3)):
+    VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
                      "tile": 128, "stages": 3,
-                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": rs}})
+                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0, "BIPB_SYMMID_T": mt,
+                              "BIPB_SYMMID_MINB": mb}})
 
 
 def name(v):
