@@ -87,6 +87,26 @@ def test_source_and_energy_parity(bp, name, make):
     ctx.close()
 
 
+@pytest.mark.parametrize("nc", [1, 511, 512, 513, 20000])
+def test_energy_launch_shapes(bp, nc):
+    """The energy launch's chunk rule (whole waves of resident CTAs, 4 charges per thread, r02) over
+    charge counts that give one partial / one full / one-plus-one charge tile and many tiles (N_c =
+    20,000 > N): per-charge phi_reac and E_sol against the oracle, and the source b."""
+    p = g.sphere_problem(4, 4.0, g.charges_in_ball(nc, 3.0, 40 + nc))
+    ctx = _ctx(bp, p)
+    b = bp.bipb_source(ctx)
+    bo = oracle.source(p)
+    assert _rel(b[:p.n], bo[:p.n]) <= 1e-12 and _rel(b[p.n:], bo[p.n:]) <= 1e-12
+    x = g.random_vector(2 * p.n, 6)
+    phi = np.zeros(p.nc)
+    e = bp.bipb_energy(ctx, x, phi)
+    ctx.close()
+    phio = oracle.reaction_potential(p, x)
+    assert _rel(phi, phio) <= 1e-12
+    assert np.max(np.abs(phi - phio)) <= 1e-12 * np.max(np.abs(phio))
+    assert e == pytest.approx(oracle.energy(p, x), rel=1e-11)
+
+
 @pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("m", [10, 20])
 @pytest.mark.parametrize("name,make", CASES[:4])
@@ -412,6 +432,32 @@ def test_matvec_batch(bp, nrhs, kappa):
     ctx.set_matvec_kernel(0)  # row kernel loops
     assert _rel(bp.bipb_matvec_batch(ctx, U), Y) <= 1e-14
     ctx.close()
+
+
+@pytest.mark.parametrize("nrhs", [2, 4])
+def test_matvec_batch_large_ragged(bp, nrhs):
+    """The multi-RHS symmetric kernels (R = 2: B = 512, R = 4: B = 384, ping-pong record buffers) on
+    a ragged N = 45,001 (many blocks, partial last block): every operand element-wise against the
+    oracle on >= 2,048 sampled rows per block (block edges of both shapes included) and in full
+    against the independently pinned row kernel."""
+    p = _ragged(6, 20.0, 45001, 17, g.charges_in_ball(10, 15.0, 6))
+    U = np.stack([g.random_vector(2 * p.n, 300 + r) for r in range(nrhs)])
+    ctx = _ctx(bp, p)
+    ctx.set_matvec_kernel(1)
+    Y = bp.bipb_matvec_batch(ctx, U)
+    ctx.set_matvec_kernel(0)
+    Y0 = bp.bipb_matvec_batch(ctx, U)
+    ctx.close()
+    edges = np.concatenate([np.arange(0, p.n + 1, 384), np.arange(0, p.n + 1, 512)])
+    rows = np.unique(np.clip(np.concatenate([edges - 1, edges, np.linspace(0, p.n - 1, 2100).astype(np.int64)]),
+                             0, p.n - 1))
+    assert rows.size >= 2048
+    for r in range(nrhs):
+        assert _rel(Y[r], Y0[r]) <= 1e-13
+        yi, yin = oracle.matvec_rows(p, U[r], rows)
+        for got, want in ((Y[r][rows], yi), (Y[r][rows + p.n], yin)):
+            assert _rel(got, want) <= 1e-11
+            assert np.max(np.abs(got - want)) <= 1e-11 * np.max(np.abs(want))
 
 
 def test_multi_rhs_charge_sets_and_batched_gmres(bp):
