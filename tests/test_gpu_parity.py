@@ -547,17 +547,21 @@ def test_gmres_graph_replay_matches_eager(bp, kind):
 
 
 def test_full_size_c5_sampled_matvec(bp):
-    """C5 (N = 1,310,720; partials launched in I-block groups): sampled rows of one product
-    against the oracle, and the symmetric and row kernels against each other."""
+    """C5 (N = 1,310,720): >= 2,048 sampled rows of one product ("row-sampled oracle
+    matvec (2,048 rows)", block edges included) against the oracle per block, rel-L2 and
+    element-wise, and the symmetric and row kernels against each other in full."""
     p = g.config("C5")
     ctx = _ctx(bp, p)
     assert ctx.matvec_kernel == 1
     u = g.random_vector(2 * p.n, 31)
     y = bp.bipb_matvec(ctx, u)
-    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 12).astype(np.int64), [0, 639, 640, p.n - 1]]))
+    rows = np.unique(np.concatenate([np.linspace(0, p.n - 1, 2048).astype(np.int64),
+                                     [0, 639, 640, 641, p.n - 641, p.n - 640, p.n - 1]]))
+    assert rows.size >= 2048
     yi, yin = oracle.matvec_rows(p, u, rows)
-    assert np.max(np.abs(y[rows] - yi)) <= 1e-11 * np.max(np.abs(yi))
-    assert np.max(np.abs(y[rows + p.n] - yin)) <= 1e-11 * np.max(np.abs(yin))
+    for got, want in ((y[rows], yi), (y[rows + p.n], yin)):
+        assert _rel(got, want) <= 1e-11
+        assert np.max(np.abs(got - want)) <= 1e-11 * np.max(np.abs(want))
     ctx.set_matvec_kernel(0)
     y0 = bp.bipb_matvec(ctx, u)
     assert _rel(y, y0) <= 1e-13
