@@ -593,11 +593,15 @@ static bipb_status sym_plan(bipb_ctx* c, bipb_ctx::SymPlan** out) {
   p.nb = cdiv(n, B);
   p.hmax = (p.nb & 1) ? (p.nb - 1) / 2 : p.nb / 2;
   bipb_partition(p.nb, c->world, c->rank, &p.I0, &p.I1);
-  const int64_t tiles_local = (p.I1 - p.I0) * (p.hmax + 1);
-  // runs of W offsets per CTA: >= 32 waves of resident CTAs (2 per SM) on this rank, W <= 4 (short
-  // CTAs of nearly equal work keep the launch's tail small; measured at C4, profiles/r01/session3/
-  // sweepW_C4.jsonl: W = 16 192.7 ms, 8 192.8, 6 191.9, 4 191.7 per product)
-  p.W = std::max<int64_t>(1, std::min<int64_t>(4, tiles_local / (148 * 2 * 32)));
+  // runs of W offsets per CTA, chosen from GLOBAL sizes only: a run's forward sums form one partial,
+  // so a W that depended on the rank's share (as in r01: >= 32 waves per rank) would group the
+  // partials differently on P ranks and the exact-sum product would differ from the single-GPU one
+  // in the last bits at large N (r02 session 4: the 8-rank C4 product).  W = 2 from 16 waves of
+  // 2 CTAs/SM per rank at 8 ranks (37,888 block pairs) on, else 1: short CTAs of nearly equal work
+  // keep the tail small on 1-8 GPUs (C4 per product: W = 1 192.5 ms, 2 191.4, 4 191.6; r01 W sweep
+  // 16 192.7, 8 192.8, 6 191.9 -- profiles/r02/session4/tune_fpo_C4.jsonl, r01/session3/sweepW_C4.jsonl)
+  const int64_t tiles_global = p.nb * (p.hmax + 1);
+  p.W = tiles_global >= (int64_t)8 * 148 * 2 * 16 ? 2 : 1;
   if (const char* e = getenv("BIPB_SYM_W")) p.W = std::max<int64_t>(1, atoll(e));  // tuning
   p.runs = cdiv(p.hmax + 1, p.W);  // an I-block's offsets split evenly over its runs (bipb_sym.cuh)
   double gb = 4.0;

@@ -280,3 +280,61 @@ def test_p2p_probe_failure_falls_back_to_nccl():
         np.testing.assert_allclose(o["b"], orc["b"], rtol=1e-12, atol=1e-14 * np.abs(orc["b"]).max())
     for o in _spawn_fail("probe_required"):
         assert o["status"] == bp.ERR_NCCL and "peer-store exchange unavailable" in o["msg"]
+
+
+def _run_product(rank, world, uid, exchange, cfg, q):
+    """One product, source and energy of a BASELINE config (no GMRES): the full-size exchange."""
+    os.environ["BIPB_NCCL_LIB"] = FAKE
+    os.environ["BIPB_GRAPHS"] = "0"
+    os.environ["BIPB_EXCHANGE"] = exchange
+    try:
+        import paper_1301_5885_b200 as bp
+        p = g.config(cfg)
+        dist = None if world == 0 else (rank, world, uid, 0)
+        ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
+        assert ctx.matvec_kernel == 1 and ctx.sum_mode == 1
+        u = g.random_vector(2 * p.n, 41)
+        y = bp.bipb_matvec(ctx, u)
+        b = bp.bipb_source(ctx)
+        e = bp.bipb_energy(ctx, u)
+        ctx.close()
+        q.put((rank, {"y": y, "b": b, "e": e}, None))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, None, repr(ex)))
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_multirank_c4_product_bitwise(exchange):
+    """The bench workload C4 (N = 327,680) over 8 ranks (an 8-GPU box's decomposition: 64 of the
+    512 I-blocks per rank, 625 charges per rank for the energy): every rank's product (exact limb
+    sums; the offset runs W come from global sizes, so the partials are the same tiles on every
+    rank count) is bitwise the single-GPU product, source and energy are equal to rounding; the
+    single-GPU product against the oracle on 256 sampled rows per block."""
+    ctx = mp.get_context("spawn")
+
+    def spawn(world):
+        q = ctx.Queue()
+        uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0") if world else None
+        procs = [ctx.Process(target=_run_product, args=(r, world, uid, exchange, "C4", q))
+                 for r in range(max(world, 1))]
+        for pr in procs:
+            pr.start()
+        res = [q.get(timeout=900) for _ in procs]
+        for pr in procs:
+            pr.join(timeout=60)
+        for _, _, err in res:
+            assert err is None, err
+        return [r[1] for r in sorted(res, key=lambda t: t[0])]
+
+    ref = spawn(0)[0]
+    outs = spawn(8)
+    p = g.config("C4")
+    for o in outs:
+        assert np.array_equal(o["y"], ref["y"])
+        assert np.linalg.norm(o["b"] - ref["b"]) <= 1e-14 * np.linalg.norm(ref["b"])
+        assert o["e"] == pytest.approx(ref["e"], rel=1e-13)
+    u = g.random_vector(2 * p.n, 41)
+    rows = np.unique(np.linspace(0, p.n - 1, 256).astype(np.int64))
+    yi, yin = oracle.matvec_rows(p, u, rows)
+    for got, want in ((ref["y"][rows], yi), (ref["y"][rows + p.n], yin)):
+        assert np.max(np.abs(got - want)) <= 1e-11 * np.max(np.abs(want))

@@ -37,12 +37,12 @@ VARIANTS = []
 # (measured: tune_sym_maxnreg_C4.jsonl, all slower; T = 6: tune_sym_t6_C4.jsonl, slower.)
 # Small problems (C1, C2): the symmetric kernel with small blocks (the mid-size shape, chosen below
 # 2,048 block pairs at B = 640, at T = 1 / 2 / 3, i.e. B = 128 / 256 / 384) against the row kernel.
-VARIANTS.append({"kind": "row", "tpb": 128, "t": 3, "minb": 3, "exp_bits": 11})
-for mt, mb in ((1, 4), (2, 4), (3, 3)):
+# (measured: profiles/r02/session4/small/tune_small_C*.jsonl -> the B = 128 small shape.)
+# Exact sums: forward partials per offset (rank-count invariant at any size) vs per run of W offsets.
+for fpo in (0, 1, 0, 1):
     VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
                      "tile": 128, "stages": 3,
-                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0, "BIPB_SYMMID_T": mt,
-                              "BIPB_SYMMID_MINB": mb}})
+                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0, "BIPB_SYM_FWD_PER_OFFSET": fpo}})
 
 
 def name(v):
