@@ -297,8 +297,11 @@ def _run_product(rank, world, uid, exchange, cfg, q):
         y = bp.bipb_matvec(ctx, u)
         b = bp.bipb_source(ctx)
         e = bp.bipb_energy(ctx, u)
+        x = np.zeros(2 * p.n)  # the bench's solve: GMRES(20) to 1e-10, one exchange per product
+        st, rep = bp.bipb_gmres_solve(ctx, x, None, 20, 1e-10, 500)
+        es = bp.bipb_energy(ctx, x)
         ctx.close()
-        q.put((rank, {"y": y, "b": b, "e": e}, None))
+        q.put((rank, {"y": y, "b": b, "e": e, "x": x, "its": rep["iterations"], "es": es, "st": st}, None))
     except Exception as ex:  # pragma: no cover
         q.put((rank, None, repr(ex)))
 
@@ -309,7 +312,9 @@ def test_multirank_c4_product_bitwise(exchange):
     512 I-blocks per rank, 625 charges per rank for the energy): every rank's product (exact limb
     sums; the offset runs W come from global sizes, so the partials are the same tiles on every
     rank count) is bitwise the single-GPU product, source and energy are equal to rounding; the
-    single-GPU product against the oracle on 256 sampled rows per block."""
+    full GMRES(20) solve on 8 ranks takes the single-GPU iteration count and matches the stored
+    oracle solve (tests/golden/oracle_C4.json: E_sol 1e-8, iterations +-1); the single-GPU
+    product against the oracle on 256 sampled rows per block."""
     ctx = mp.get_context("spawn")
 
     def spawn(world):
@@ -329,10 +334,18 @@ def test_multirank_c4_product_bitwise(exchange):
     ref = spawn(0)[0]
     outs = spawn(8)
     p = g.config("C4")
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_C4.json")))
+    assert gold["sha256"] == p.sha256()
+    s20 = gold["solves"]["20"]
     for o in outs:
         assert np.array_equal(o["y"], ref["y"])
         assert np.linalg.norm(o["b"] - ref["b"]) <= 1e-14 * np.linalg.norm(ref["b"])
         assert o["e"] == pytest.approx(ref["e"], rel=1e-13)
+        # the full solve on 8 ranks: the single-GPU iteration, and the stored oracle solve
+        assert o["st"] == 0 and o["its"] == ref["its"]
+        assert np.linalg.norm(o["x"] - ref["x"]) <= 1e-12 * np.linalg.norm(ref["x"])
+        assert abs(o["its"] - s20["iterations"]) <= 1
+        assert o["es"] == pytest.approx(s20["energy"], rel=1e-8)
     u = g.random_vector(2 * p.n, 41)
     rows = np.unique(np.linspace(0, p.n - 1, 256).astype(np.int64))
     yi, yin = oracle.matvec_rows(p, u, rows)
