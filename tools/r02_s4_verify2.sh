@@ -2,7 +2,7 @@
 # r02 session 4: the small block shape (B = 128) and the new default-kernel rule -- whole GPU suite,
 # smoke, C1/C2/C4 benches.
 set -u
-O=gpurun_out/s4m
+O=gpurun_out/${TAG:-s4m}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -1 $O/smoke.txt
