@@ -25,7 +25,9 @@ FAKE = os.path.join(os.path.dirname(__file__), "fakenccl", "libfakenccl.so")
 def _problem(size="big"):
     if size == "tiny":  # 20 elements, 3 charges: most ranks own no rows, blocks or charges
         return g.sphere_problem(0, 4.0, g.charges_in_ball(3, 2.0, 5))
-    return g.config("C2")  # N = 20480 (symmetric default), the stored oracle solve exists
+    if size == "c1":  # N = 5120: the symmetric kernel's small block shape (B = 128, r02)
+        return g.config("C1")
+    return g.config("C2")  # N = 20480 (symmetric default, B = 384), the stored oracle solve exists
 
 
 _ORC = {}
@@ -42,7 +44,8 @@ def _oracle(size):
             o.update(e=oracle.energy(p, x), its=rep["iterations"], rows=np.arange(p.n), x_phi=x[:p.n],
                      x_dphi=x[p.n:], x_norm=float(np.linalg.norm(x)))
         else:
-            gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_C2.json")))
+            gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                               "oracle_C1.json" if size == "c1" else "oracle_C2.json")))
             assert gold["sha256"] == p.sha256()
             s20 = gold["solves"]["20"]
             o.update(e=s20["energy"], its=s20["iterations"], rows=np.array(s20["rows"]),
@@ -159,9 +162,8 @@ def test_multirank_tiny_problem(kind, exchange):
         assert o["e"] == pytest.approx(ref["e"], rel=1e-12)
 
 
-@pytest.mark.parametrize("size", ["big", "tiny"])
-@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
-@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("world,exchange,size", [(w, x, s) for s in ("big", "tiny") for x in ("nccl", "p2p")
+                                                  for w in (2, 3, 8)] + [(8, "p2p", "c1"), (3, "nccl", "c1")])
 def test_multirank_exact_sums_bitwise(world, exchange, size):
     """Exact limb sums (bipb_set_sum_mode 1): the symmetric product, the replicated GMRES and the
     energy are bitwise the single-GPU results for every rank count and both exchanges."""
@@ -282,8 +284,8 @@ def test_p2p_probe_failure_falls_back_to_nccl():
         assert o["status"] == bp.ERR_NCCL and "peer-store exchange unavailable" in o["msg"]
 
 
-def _run_product(rank, world, uid, exchange, cfg, q):
-    """One product, source and energy of a BASELINE config (no GMRES): the full-size exchange."""
+def _run_product(rank, world, uid, exchange, cfg, q, kind=1):
+    """Product, source, energy and the full GMRES solve of a BASELINE config: the full-size exchange."""
     os.environ["BIPB_NCCL_LIB"] = FAKE
     os.environ["BIPB_GRAPHS"] = "0"
     os.environ["BIPB_EXCHANGE"] = exchange
@@ -293,6 +295,7 @@ def _run_product(rank, world, uid, exchange, cfg, q):
         dist = None if world == 0 else (rank, world, uid, 0)
         ctx = bp.bipb_setup(p.centroids, p.normals, p.areas, p.charges, p.eps1, p.eps2, p.kappa, dist=dist)
         assert ctx.matvec_kernel == 1 and ctx.sum_mode == 1
+        ctx.set_matvec_kernel(kind)  # 0: the row kernel (rank-count invariant chunk sums)
         u = g.random_vector(2 * p.n, 41)
         y = bp.bipb_matvec(ctx, u)
         b = bp.bipb_source(ctx)
@@ -306,8 +309,8 @@ def _run_product(rank, world, uid, exchange, cfg, q):
         q.put((rank, None, repr(ex)))
 
 
-@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
-def test_multirank_c4_product_bitwise(exchange):
+@pytest.mark.parametrize("kind,exchange", [(1, "p2p"), (1, "nccl"), (0, "p2p")])
+def test_multirank_c4_product_bitwise(kind, exchange):
     """The bench workload C4 (N = 327,680) over 8 ranks (an 8-GPU box's decomposition: 64 of the
     512 I-blocks per rank, 625 charges per rank for the energy): every rank's product (exact limb
     sums; the offset runs W come from global sizes, so the partials are the same tiles on every
@@ -320,7 +323,7 @@ def test_multirank_c4_product_bitwise(exchange):
     def spawn(world):
         q = ctx.Queue()
         uid = f"/bipb_fakenccl_{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0") if world else None
-        procs = [ctx.Process(target=_run_product, args=(r, world, uid, exchange, "C4", q))
+        procs = [ctx.Process(target=_run_product, args=(r, world, uid, exchange, "C4", q, kind))
                  for r in range(max(world, 1))]
         for pr in procs:
             pr.start()
