@@ -93,9 +93,14 @@ def _run(rank, world, uid, kind, exchange, q, size="big", sum_mode="fixed"):
         ctx.set_precond(1)  # the opt-in preconditioned solve (replicated like the plain one)
         xp = np.zeros(2 * p.n)
         st, repp = bp.bipb_gmres_solve(ctx, xp, None, 20, 1e-10, 300)
+        ctx.set_precond(0)
+        # lockstep batched GMRES (multi-RHS, one shared product per step): b and 3b -> x and 3x
+        XB = np.zeros((2, 2 * p.n))
+        stb, repb = bp.bipb_gmres_solve_batch(ctx, np.stack([b, 3.0 * b]), XB, 20, 1e-10, 300)
         ctx.close()
         q.put((rank, {"y": y, "Y": Y, "b": b, "x": x, "its": rep["iterations"], "e": e, "phi": phi, "xp": xp,
-                      "its_p": repp["iterations"]}, None))
+                      "its_p": repp["iterations"], "XB": XB, "its_b": [r["iterations"] for r in repb],
+                      "st_b": stb}, None))
     except Exception as ex:  # pragma: no cover
         q.put((rank, None, repr(ex)))
 
@@ -143,6 +148,11 @@ def test_multirank_matches_single(world, kind, exchange):
             assert np.array_equal(o["b"], ref["b"])
             assert rel(o["x"], ref["x"]) <= 1e-11 and o["e"] == pytest.approx(ref["e"], rel=1e-12)
         np.testing.assert_allclose(o["phi"], ref["phi"], rtol=1e-13, atol=1e-16)
+        # batched GMRES on P ranks: replicated, equal to the single-GPU batch and to the plain solve
+        assert o["st_b"] == 0 and o["its_b"] == ref["its_b"]
+        assert np.array_equal(o["XB"], outs[0]["XB"])
+        assert rel(o["XB"], ref["XB"]) <= 1e-11
+        assert rel(o["XB"][0], o["x"]) <= 1e-9 and rel(o["XB"][1], 3.0 * o["x"]) <= 1e-9
 
 
 @pytest.mark.parametrize("exchange", ["nccl", "p2p"])
