@@ -35,6 +35,22 @@ def test_reference_arm_json():
     assert d["config"] == json.loads(json.dumps(bench.bench_config(g.config("C1"), 1)))
 
 
+def test_golden_check_logic():
+    """bench.golden_check: matched by input SHA-256, tolerance north_star's (1e-8, +-1 iteration);
+    a config without a stored solve (C5) or another input gives no entry."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import bipb_inputs as g
+    p = g.config("C2")
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_C2.json")))["solves"]["20"]
+    ok = bench.golden_check(p, gold["energy"] * (1 + 5e-9), gold["iterations"] + 1)
+    assert ok["pass"] and ok["file"].endswith("oracle_C2.json") and ok["iterations_diff"] == 1
+    assert not bench.golden_check(p, gold["energy"] * (1 + 2e-8), gold["iterations"])["pass"]
+    assert not bench.golden_check(p, gold["energy"], gold["iterations"] + 2)["pass"]
+    q = g.Problem(p.name, p.centroids, p.normals, p.areas, p.charges, 2.0, p.eps2, p.kappa)  # another input
+    assert bench.golden_check(q, gold["energy"], gold["iterations"]) is None
+
+
 @pytest.mark.gpu
 def test_native_arm_json():
     d = _run(["--config", "C2", "--steps", "1", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "2",
