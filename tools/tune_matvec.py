@@ -39,17 +39,20 @@ VARIANTS = []
 # 2,048 block pairs at B = 640, at T = 1 / 2 / 3, i.e. B = 128 / 256 / 384) against the row kernel.
 # (measured: profiles/r02/session4/small/tune_small_C*.jsonl -> the B = 128 small shape.)
 # Exact sums: forward partials per offset (rank-count invariant at any size) vs per run of W offsets.
-for fpo in (0, 1, 0, 1):
+# (measured: tune_fpo_C4.jsonl; the rank invariance came from a global W instead.)  ptxas options
+# (the same source scheduled differently): -O2, -O1, --allow-expensive-optimizations.
+for px in ([], ["-Xptxas", "-O2"], ["-Xptxas", "-O1"], ["-Xptxas", "--allow-expensive-optimizations=true"], []):
     VARIANTS.append({"kind": "sym", "tpb": 128, "t": 5, "minb": 1, "exp_bits": 11, "pf": 1, "un": 1,
-                     "tile": 128, "stages": 3,
-                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0, "BIPB_SYM_FWD_PER_OFFSET": fpo}})
+                     "tile": 128, "stages": 3, "ptxas": px,
+                     "defs": {"BIPB_SYM_STUNROLL": 1, "BIPB_SYM_RS_STAGE": 0}})
 
 
 def name(v):
     extra = "".join(f"_{k.replace('BIPB_', '').lower()}{val}" for k, val in sorted(v.get("defs", {}).items()))
     return (f"{v.get('kind', 'row')}_tpb{v['tpb']}_t{v['t']}_minb{v['minb']}_eb{v['exp_bits']}_pf{v.get('pf', 0)}"
             f"_un{v.get('un', 1)}_tile{v.get('tile', 128)}_st{v.get('stages', 3)}{extra}"
-            + (f"_mr{v['maxrreg']}" if v.get("maxrreg") else ""))
+            + (f"_mr{v['maxrreg']}" if v.get("maxrreg") else "")
+            + "".join("_" + a.strip("-").split("=")[0] for a in v.get("ptxas", []) if a != "-Xptxas"))
 
 
 def build():
@@ -68,6 +71,7 @@ def build():
             extra += [f"-D{k}={val}" for k, val in v.get("defs", {}).items()]
             if v.get("maxrreg"):
                 extra += [f"-DBIPB_SYM_MAXNREG={v['maxrreg']}"]
+            extra += v.get("ptxas", [])
         else:
             extra = [f"-DBIPB_MV_TPB={v['tpb']}", f"-DBIPB_MV_T={v['t']}", f"-DBIPB_MV_MINB={v['minb']}",
                      f"-DBIPB_EXP_BITS={v['exp_bits']}"]
